@@ -1,0 +1,402 @@
+"""Benchmark: GPU-PB tree advance (state*vocab/s) and boosted-decode RTFx on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Headline (`value`): tree-advance cells/s (one cell = one (state, token)
+pair resolved: f32 score + i32 next state written), BASELINE config 5:
+20K-phrase tree (default_rng(1008) corpus, V=1024) replicated on every
+GPU, 8192 states per GPU per step (weak scaling: each rank shards its own
+8192 utterance states; no data-path collective).  A step is one advance
+launch over one resident batch of states; outputs rotate through a ring
+of 4 x 64 MiB buffers (256 MiB > 126 MB L2), so every step's writes reach
+HBM.  `e2e`: same metric through the public API with host numpy buffers
+(get_scores_batch: H2D states, kernel, D2H of both [B,V] outputs).
+`decode`: boosted vs unboosted fused greedy CTC RTFx (20K tree, V=1024,
+batch 128 x 200 frames of synthetic log-probs), device-timed.
+`cpu_baseline`: the reference's own compiled kernel (oracle/_ref, built
+from /root/reference's _kernels.pyx) on the host cores, bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+METRIC = "boosted-decode RTFx and tree-advance state·vocab/s at 20K phrases, 1/2/4/8 B200"
+UNIT = "state*vocab/s"
+B_PER_GPU = 8192
+CORPUS = "p20k_v1024"
+RING = 4
+FRAME_SEC = 0.04  # acoustic.py:35
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=B_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def build_table():
+    import gen_inputs as gi
+
+    import paper_2508_07014_b200 as pb
+
+    phrases, V = gi.corpus(CORPUS)
+    ctx = pb.ContextList([pb.Phrase(" ".join(map(str, p)), p) for p in phrases], min_chars=0)
+    tab = pb.compile_arc_table(pb.compute_fail_links(pb.build_prefix_tree(ctx, pb.TreeParams(), V)))
+    return tab, phrases, V
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        util = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    p = ROOT / "profiles" / "advance_ncu_summary.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_07014_b200 as pb
+    from paper_2508_07014_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    tab, phrases, V = build_table()
+    S = tab.num_states
+    B = args.batch
+    dtab = tab.device_table(local)
+    # resident inputs: a ring of state batches (each rank its own shard of utterances)
+    rng = np.random.default_rng(1000 + rank)
+    n_in = max(args.steps, 8)
+    states = torch.from_numpy(rng.integers(0, S, size=(n_in, B)).astype(np.int32)).to(dev)
+    outs = [(torch.empty((B, V), dtype=torch.float32, device=dev), torch.empty((B, V), dtype=torch.int32, device=dev))
+            for _ in range(RING)]
+    stream = torch.cuda.current_stream(dev)
+    sp = int(stream.cuda_stream)
+
+    def step(i):
+        s, n = outs[i % RING]
+        _lib.check(_lib.LIB.pgpb_advance(dtab.handle, states[i % n_in].data_ptr(), B, s.data_ptr(), n.data_ptr(), sp))
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step(i)
+            ev[i][1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = start.elapsed_time(stop)
+    per_launch = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = statistics.mean(per_launch)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_max = float(t.item())
+    cells_total = float(B) * V * args.steps * world
+    value = cells_total / (ms_max / 1e3)
+
+    # correctness spot check of the timed outputs (last ring slot) vs table semantics
+    # is covered by tests; here only make sure nothing failed
+    torch.cuda.synchronize(dev)
+
+    # e2e through the public API with host buffers
+    e2e_states = [rng.integers(0, S, size=B).astype(np.int32) for _ in range(4)]
+    for i in range(2):
+        pb.get_scores_batch(tab, e2e_states[i % 4])
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        r = pb.get_scores_batch(tab, e2e_states[i % 4])
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = float(B) * V * e2e_steps * world / float(te.item())
+    del r
+
+    hbm_peak, peak_kind = peaks()
+    bytes_alg = float(B) * V * 8 + B * 4
+    achieved = bytes_alg / (kern_ms / 1e3) / 1e9
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32+i32 (fp32 scores, int32 next states)",
+        "data": "synthetic (seeded 20K-phrase corpus, uniform random states)",
+        "config": {
+            "workload": "config5: tree advance, 8192 states/GPU x 20K-phrase tree (S=%d) x V=%d, table replicated" % (S, V),
+            "states_per_gpu": B, "vocab": V, "num_states": S, "phrases": len(phrases),
+            "parallelism": f"dp{world} (utterance-state shards, replicated table)",
+            "l2": "outputs rotate over 4x%d MiB ring (> 126 MB L2)" % (B * V * 8 // 2**20),
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic(), "peak_kind": peak_kind,
+                     "kernel": "advance_closure_kernel", "bytes_alg_per_launch": bytes_alg,
+                     "kernel_ms": kern_ms},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": B * V * 8,
+                "api": "paper_2508_07014_b200.get_scores_batch(numpy) -> C-ABI pgpb_advance_host"},
+        "gpu_launches": args.steps + e2e_steps,
+        "clocks": clk.summary(),
+    }
+    if not args.no_decode:
+        out["decode"] = bench_decode(tab, V, dev, rank, world)
+        out["gpu_launches"] += out["decode"].pop("_launches", 0)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(tab, B, V)
+    return out
+
+
+def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=5):
+    """Device-timed fused greedy CTC: boosted vs unboosted RTFx (audio = B*T*0.04 s)."""
+    import torch
+
+    import gen_inputs as gi  # noqa: F401
+    import paper_2508_07014_b200 as pb
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    logits = torch.randn((B, T, V), generator=g, device=dev) * 2.0
+    lp = torch.log_softmax(logits, dim=-1).contiguous()
+    del logits
+    res = {}
+    launches = 0
+    for name, cfg in (("unboosted", pb.DecodeConfig(lam=0.0)), ("boosted", pb.DecodeConfig(lam=1.0))):
+        o = pb.ctc_greedy_device(lp, None, tab, cfg, 0)
+        torch.cuda.synchronize(dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            o = pb.ctc_greedy_device(lp, None, tab, cfg, 0, out=o)
+        e.record()
+        torch.cuda.synchronize(dev)
+        launches += reps
+        ms = s.elapsed_time(e) / reps
+        res[name] = {"ms": ms, "rtfx": B * T * FRAME_SEC / (ms / 1e3) * world}
+    res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
+    res["workload"] = f"greedy CTC, batch {B} x {T} frames, V={V}, 20K-phrase tree, lam=1 vs 0"
+    res["_launches"] = launches
+    return res
+
+
+def _ref_module():
+    from oracle import oracle as orc
+
+    mod = orc.ref_kernels()
+    return (mod, "reference") if mod is not None else (None, "port")
+
+
+def _cpu_advance(tab, states, threads):
+    """Advance on host cores: reference kernel (oracle/_ref) or the oracle port,
+    batch sharded over a thread pool (the kernels release the GIL), as the
+    reference CLI's --workers pool does (cli.py:302-310)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as orc
+
+    mod, kind = _ref_module()
+    arrs = orc._tab_arrays(tab)
+    shards = np.array_split(states, threads)
+    if mod is not None:
+        fn = lambda s: mod.score_batch(*arrs, np.ascontiguousarray(s))  # noqa: E731
+    else:
+        fn = lambda s: orc.score_batch(tab, s)  # noqa: E731
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(fn, shards))
+    return kind
+
+
+def cpu_baseline(tab, B, V, budget_s=10.0):
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(7)
+    st = rng.integers(0, tab.num_states, size=B).astype(np.int32)
+    kind = _cpu_advance(tab, st, threads)  # warm-up
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        _cpu_advance(tab, st, threads)
+        n += 1
+    el = time.perf_counter() - t0
+    return {"value": n * B * V / el, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{n} full advances of {B} states x V={V} (20K tree) in {el:.1f}s, "
+                      f"batch sharded over {threads} threads",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    tab, phrases, V = build_table()
+    B = args.batch
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(1000)
+    st = [rng.integers(0, tab.num_states, size=B).astype(np.int32) for _ in range(4)]
+    for i in range(args.warmup):
+        kind = _cpu_advance(tab, st[i % 4], threads)
+    kind = _ref_module()[1]
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        _cpu_advance(tab, st[i % 4], threads)
+    el = time.perf_counter() - t0
+    value = args.steps * B * V / el
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic (seeded 20K-phrase corpus, uniform random states)",
+        "config": {"workload": "config5: tree advance, %d states x 20K-phrase tree x V=%d on host cores" % (B, V),
+                   "states_per_step": B, "vocab": V, "num_states": tab.num_states},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"each step = one full {B}-state advance sharded over {threads} threads",
+                         "cpu_model": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    out = run_ours(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+/*
+ * pgpb.h — C-ABI of the B200-native GPU phrase-boosting tree (GPU-PB).
+ *
+ * This is the drop-in boundary for the reference's native kernel module
+ * (`phraseboost._kernels`, /root/reference/pkg/src/phraseboost/_kernels.pyx)
+ * and for the host-side tree compiler the reference implements in Python
+ * (tree.py / table.py).  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *   - Every entry point returns PGPB_OK (0) or a negative PGPB_E* code; the
+ *     message of the last failure on the calling thread is available from
+ *     pgpb_last_error().  (The reference raises Python exceptions instead;
+ *     the Python host layer maps these codes back to the reference's
+ *     exception types and messages.)
+ *   - `d_` pointers are device pointers, `h_` pointers host pointers.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *     All device work is stream-ordered; nothing synchronises unless the
+ *     function name ends in `_host` (those copy results back and wait).
+ *   - The caller owns every buffer it passes in; a pgpb_table owns its own
+ *     device copy of the compiled arc table and is immutable after creation,
+ *     so one table may be used concurrently from many streams / threads
+ *     (reference: SPEC.md:259, tests/test_table.py:330-343).
+ */
+#ifndef PGPB_H
+#define PGPB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGPB_ABI_VERSION 1
+
+#define PGPB_OK 0
+#define PGPB_EINVAL (-1)     /* bad argument (maps to ValueError)            */
+#define PGPB_ERANGE (-2)     /* index out of range (maps to IndexError)       */
+#define PGPB_ECUDA (-3)      /* CUDA runtime failure                          */
+#define PGPB_ENOMEM (-4)     /* allocation failure                            */
+#define PGPB_EFORMAT (-5)    /* table invariant violated (TableFormatError)   */
+
+#define PGPB_WEIGHT_DEPTH_SCALED 0 /* tree.py:30 */
+#define PGPB_WEIGHT_UNIFORM 1      /* tree.py:31 */
+
+const char *pgpb_last_error(void);
+int pgpb_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * Tree compilation (host code, C++).  Replaces the Python loops of
+ *   build_prefix_tree   tree.py:145-186
+ *   compute_fail_links  tree.py:189-214
+ *   compile_arc_table   table.py:138-187
+ * Node ids follow the reference exactly (creation order while inserting
+ * phrases in ContextList order, root = 0), so next-state ids are
+ * bit-identical to the reference's.
+ * ---------------------------------------------------------------------- */
+
+/* build_prefix_tree (tree.py:145-186).  Phrases are given as CSR:
+ * tokens[offsets[i] .. offsets[i+1]) is phrase i.  `capacity` is the size of
+ * every node output array (1 + offsets[n_phrases] always suffices).
+ * On an empty phrase or an out-of-range token returns PGPB_EINVAL and sets
+ * *bad_phrase (and *bad_token, -1 for "empty").                            */
+int pgpb_trie_build(const int32_t *h_tokens, const int64_t *h_offsets, int64_t n_phrases,
+                    int32_t vocab_size, double c0, double beta, int32_t weight_mode,
+                    double uniform_final_bonus, int64_t capacity, int32_t *h_parent,
+                    int32_t *h_depth, int32_t *h_in_token, uint8_t *h_is_final,
+                    double *h_arc_score, double *h_acc_score, int64_t *num_nodes,
+                    int64_t *bad_phrase, int64_t *bad_token);
+
+/* compute_fail_links (tree.py:189-214): Aho-Corasick longest proper suffix.
+ * Writes fail[num_nodes] (fail[0] = 0).                                    */
+int pgpb_trie_fail_links(int64_t num_nodes, const int32_t *h_parent, const int32_t *h_in_token,
+                         int32_t vocab_size, int32_t *h_fail);
+
+/* compile_arc_table (table.py:138-187).  Arc arrays have num_nodes-1
+ * entries, sorted by (from, token); state arrays have num_nodes entries.
+ * fp64 -> fp32 rounding points follow table.py:158, :163-169.               */
+int pgpb_trie_compile(int64_t num_nodes, const int32_t *h_parent, const int32_t *h_in_token,
+                      const uint8_t *h_is_final, const double *h_arc_score,
+                      const double *h_acc_score, const int32_t *h_fail, int32_t *h_arc_from,
+                      int32_t *h_arc_token, int32_t *h_arc_to, float *h_arc_weight,
+                      int32_t *h_state_start, int32_t *h_state_end, int32_t *h_backoff_to,
+                      float *h_backoff_weight, float *h_final_score);
+
+/* ------------------------------------------------------------------------
+ * Device-resident compiled table.
+ * Takes the reference ArcTable arrays (table.py:53-69, the 9 arrays the
+ * reference passes to score_batch plus is_final / final_score) and builds
+ * the device layout described in DESIGN.md §3: dense root row, packed
+ * 16-byte state records and arcs, and the per-state flattened backoff
+ * closure.  Validates chain termination (PGPB_EFORMAT on a backoff cycle).
+ * ---------------------------------------------------------------------- */
+typedef struct pgpb_table pgpb_table;
+
+typedef struct pgpb_table_info {
+  int32_t num_states;
+  int32_t vocab_size;
+  int32_t num_arcs;
+  int32_t max_chain;        /* longest backoff chain (states, excluding root) */
+  int64_t closure_entries;  /* total flattened first-hit arcs over all states */
+  int32_t max_closure;      /* largest per-state closure                       */
+  int32_t device;
+  int64_t device_bytes;     /* HBM held by the table                           */
+  float unk_score;
+  float max_root_score;
+} pgpb_table_info;
+
+int pgpb_table_create(int32_t num_states, int32_t vocab_size, int32_t num_arcs,
+                      const int32_t *h_arc_token, const int32_t *h_arc_to,
+                      const float *h_arc_weight, const int32_t *h_state_start,
+                      const int32_t *h_state_end, const int32_t *h_backoff_to,
+                      const float *h_backoff_weight, const uint8_t *h_is_final,
+                      const float *h_final_score, float unk_score, int32_t device,
+                      pgpb_table **out);
+int pgpb_table_info_get(const pgpb_table *table, pgpb_table_info *out);
+void pgpb_table_destroy(pgpb_table *table);
+
+/* ------------------------------------------------------------------------
+ * Advance = get_scores_batch (table.py:190-214) / _kernels.score_batch
+ * (_kernels.pyx:30-72): for each of B states, the boosting score and next
+ * state of every token.  scores[B,V] f32 and next[B,V] i32, C order.
+ * Bit-exact with the reference (fp32 accumulation in backoff-chain order,
+ * first hit wins).  States are NOT range-checked on device (the reference
+ * kernel does not either, _kernels.pyx:1); the host layer raises IndexError
+ * as table.py:198-199 does.  B = 0 is a no-op.
+ * ---------------------------------------------------------------------- */
+int pgpb_advance(const pgpb_table *table, const int32_t *d_states, int64_t batch,
+                 float *d_scores, int32_t *d_next, void *stream);
+
+/* Same, host buffers in and out: H2D of the states, the kernel, D2H of both
+ * outputs, then a stream synchronize — the exact contract of
+ * _kernels.score_batch (fresh C-order [B,V] outputs the caller allocated).
+ * Range-checks states (PGPB_ERANGE).                                       */
+int pgpb_advance_host(const pgpb_table *table, const int32_t *h_states, int64_t batch,
+                      float *h_scores, int32_t *h_next, void *stream);
+
+/* Reference chain-walk advance (no flattened closure): walks failure arcs
+ * per row exactly as _kernels.pyx:56-71.  Same outputs as pgpb_advance;
+ * kept for tables whose closure would not fit and as a cross-check.        */
+int pgpb_advance_chain(const pgpb_table *table, const int32_t *d_states, int64_t batch,
+                       float *d_scores, int32_t *d_next, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Fused batched greedy CTC = _kernels.ctc_greedy (_kernels.pyx:75-225) /
+ * ctc_greedy_boosted (decoding.py:156-229), over B utterances at once.
+ * logprobs [B,T,V] f32 C order; lengths[B] (<= T) frames per utterance.
+ * table may be NULL (boost inactive, decoding.py:103-104); otherwise
+ * use_boost selects the boosted path.  The [B,V] score matrix is never
+ * materialised.  Outputs (device):
+ *   tokens[B,T] i32, deltas[B,T] f64, states[B,T] i32  (first num_out[b]
+ *   entries of row b valid), num_out[B] i32, am[B] f64, boost[B] f64.
+ * Results per utterance are bit-identical to the reference's per-utterance
+ * call (fp64 fusion without FMA, tie-breaks: combined, raw logprob, id).    */
+int pgpb_ctc_greedy(const pgpb_table *table, const float *d_logprobs, int64_t batch,
+                    int64_t max_frames, int32_t vocab_size, const int32_t *d_lengths,
+                    int32_t blank, double lam, int32_t use_boost, int32_t *d_tokens,
+                    double *d_deltas, int32_t *d_states, int32_t *d_num_out, double *d_am,
+                    double *d_boost, void *stream);
+
+/* Host-buffer form of one utterance, the exact contract of
+ * _kernels.ctc_greedy: h_logprobs [T,V]; outputs sized T; *num_out set.     */
+int pgpb_ctc_greedy_host(const pgpb_table *table, const float *h_logprobs, int64_t frames,
+                         int32_t vocab_size, int32_t blank, double lam, int32_t use_boost,
+                         int32_t *h_tokens, double *h_deltas, int32_t *h_states,
+                         int64_t *num_out, double *h_am, double *h_boost, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Fused boosted greedy step for transducers (RNN-T / TDT label looping):
+ * the body of transducer_greedy_boosted's inner loop (decoding.py:373-392)
+ * for B rows at once.  For each row r with active[r] != 0:
+ *   a = first argmax of logprobs[r,:];  is_blank[r] = (a == blank)
+ *   if !is_blank: chosen = boosted rerank excluding blank only (R7/R6
+ *   tie-breaks), delta = tree score, next = tree next state (when boost is
+ *   off: chosen = a, delta = 0, next = 0).
+ * Writes chosen[r] (= a when blank), lp_chosen[r] (f32 logprob of chosen),
+ * delta[r] f64, next_state[r].  Inactive rows are left untouched.
+ * ld = row stride of logprobs in elements.                                  */
+int pgpb_greedy_step(const pgpb_table *table, const float *d_logprobs, int64_t ld,
+                     int64_t rows, int32_t vocab_size, const int32_t *d_states,
+                     const uint8_t *d_active, int32_t blank, double lam, int32_t use_boost,
+                     int32_t *d_chosen, float *d_lp_chosen, double *d_delta,
+                     int32_t *d_next_state, uint8_t *d_is_blank, void *stream);
+
+/* Per-state maximum of the resolved score row, max_v scores[s, v]
+ * (used by the AED eos bump, decoding.py:546-552).  out[S] f32.             */
+int pgpb_row_max(const pgpb_table *table, float *d_out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Fused beam expansion (the V-wide inner loops of the reference's beam
+ * decoders: ctc_beam_boosted decoding.py:294-321, transducer_beam_boosted
+ * :473-489, aed_beam_boosted :544-583).  Hypotheses come in groups of
+ * `group` consecutive rows (one utterance each, padded rows have
+ * valid[h] == 0).  Every candidate (h, v) with v != exclude[h] is scored
+ *      am'    = base(h, v) + (double)lp[h, v]
+ *               base = alt_am[h] if v == alt_token[h] else am[h]
+ *      boost' = boost[h] + (double)score[state[h], v]      (0 if !use_boost)
+ *      key    = am' + lam * boost'      (fp64, unfused; decoding.py:323-327)
+ * and the best `k` (<= 32) per group are returned ordered by key desc,
+ * am' desc, then (h, v) ascending.  With skip_neg_inf, candidates whose am'
+ * is -inf are dropped (decoding.py:303-304).  The [H,V] score matrix is
+ * never materialised.  Outputs are [G, k]; unfilled slots get hyp = -1.
+ * alt_token / alt_am / valid may be NULL.  ld = 0 broadcasts one row to all
+ * hypotheses (CTC prefix beam: every prefix reads the same frame).         */
+int pgpb_beam_topk(const pgpb_table *table, const float *d_logprobs, int64_t ld,
+                   int64_t hyps, int32_t vocab_size, int32_t group, int32_t k,
+                   const int32_t *d_states, const double *d_am, const double *d_boost,
+                   const int32_t *d_exclude, const int32_t *d_alt_token,
+                   const double *d_alt_am, const uint8_t *d_valid, double lam,
+                   int32_t use_boost, int32_t skip_neg_inf, int32_t *d_out_hyp,
+                   int32_t *d_out_token, double *d_out_am, double *d_out_boost,
+                   int32_t *d_out_next, float *d_out_delta, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGPB_H */

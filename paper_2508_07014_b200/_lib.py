@@ -1,0 +1,146 @@
+"""ctypes binding of the C-ABI library libpgpb.so (include/pgpb.h).
+
+The product path has no CPU fallback: importing this module on a machine
+where libpgpb.so is missing raises immediately, and every compute entry
+point needs a CUDA device.  Error codes from the library are mapped to the
+reference's exception types (ValueError / IndexError / TableFormatError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_uint8, c_void_p
+from pathlib import Path
+
+import numpy as np
+
+from .errors import TableFormatError
+
+LIB_PATH = Path(__file__).resolve().parent / "libpgpb.so"
+
+PGPB_OK = 0
+PGPB_EINVAL = -1
+PGPB_ERANGE = -2
+PGPB_ECUDA = -3
+PGPB_ENOMEM = -4
+PGPB_EFORMAT = -5
+
+
+class TableInfo(ctypes.Structure):
+    _fields_ = [
+        ("num_states", c_int32),
+        ("vocab_size", c_int32),
+        ("num_arcs", c_int32),
+        ("max_chain", c_int32),
+        ("closure_entries", c_int64),
+        ("max_closure", c_int32),
+        ("device", c_int32),
+        ("device_bytes", c_int64),
+        ("unk_score", c_float),
+        ("max_root_score", c_float),
+    ]
+
+
+# name -> argtypes (all return int unless listed in _VOID / _OTHER)
+_P = c_void_p
+_SIGS = {
+    "pgpb_abi_version": [],
+    "pgpb_trie_build": [_P, _P, c_int64, c_int32, c_double, c_double, c_int32, c_double, c_int64,
+                        _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "pgpb_trie_fail_links": [c_int64, _P, _P, c_int32, _P],
+    "pgpb_trie_compile": [c_int64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "pgpb_table_create": [c_int32, c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_float,
+                          c_int32, POINTER(c_void_p)],
+    "pgpb_table_info_get": [c_void_p, POINTER(TableInfo)],
+    "pgpb_advance": [c_void_p, _P, c_int64, _P, _P, c_void_p],
+    "pgpb_advance_host": [c_void_p, _P, c_int64, _P, _P, c_void_p],
+    "pgpb_advance_chain": [c_void_p, _P, c_int64, _P, _P, c_void_p],
+    "pgpb_ctc_greedy": [c_void_p, _P, c_int64, c_int64, c_int32, _P, c_int32, c_double, c_int32,
+                        _P, _P, _P, _P, _P, _P, c_void_p],
+    "pgpb_ctc_greedy_host": [c_void_p, _P, c_int64, c_int32, c_int32, c_double, c_int32, _P, _P, _P,
+                             _P, _P, _P, c_void_p],
+    "pgpb_greedy_step": [c_void_p, _P, c_int64, c_int64, c_int32, _P, _P, c_int32, c_double, c_int32,
+                         _P, _P, _P, _P, _P, c_void_p],
+    "pgpb_row_max": [c_void_p, _P, c_void_p],
+    "pgpb_beam_topk": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_int32, _P, _P, _P, _P,
+                       _P, _P, _P, c_double, c_int32, c_int32, _P, _P, _P, _P, _P, _P, c_void_p],
+}
+
+# Every symbol include/pgpb.h declares (checked by tests/test_abi.py).
+EXPORTED = sorted(list(_SIGS) + ["pgpb_last_error", "pgpb_table_destroy"])
+
+
+def _load() -> ctypes.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA extension first "
+            "(python -m paper_2508_07014_b200._build); there is no CPU fallback"
+        )
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = c_int32
+    lib.pgpb_last_error.argtypes = []
+    lib.pgpb_last_error.restype = ctypes.c_char_p
+    lib.pgpb_table_destroy.argtypes = [c_void_p]
+    lib.pgpb_table_destroy.restype = None
+    return lib
+
+
+LIB = _load()
+
+
+def last_error() -> str:
+    msg = LIB.pgpb_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    """Raise the reference-equivalent exception for a library error code."""
+    if rc == PGPB_OK:
+        return
+    msg = last_error() or what
+    if rc == PGPB_ERANGE:
+        raise IndexError(msg)
+    if rc == PGPB_EINVAL:
+        raise ValueError(msg)
+    if rc == PGPB_EFORMAT:
+        raise TableFormatError(msg)
+    if rc == PGPB_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"pgpb CUDA error: {msg}")
+
+
+def ptr(a) -> int | None:
+    """Data pointer of a contiguous numpy array or torch tensor (None if None)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("ndarray is not C-contiguous")
+        return a.ctypes.data
+    if not a.is_contiguous():
+        raise ValueError("tensor is not contiguous")
+    return a.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    """cudaStream_t of `stream` (or torch's current stream) as an int."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def require_cuda() -> None:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_2508_07014_b200 needs a CUDA device (sm_100a); there is no CPU fallback"
+        )
+
+
+def abi_version() -> int:
+    return int(LIB.pgpb_abi_version())

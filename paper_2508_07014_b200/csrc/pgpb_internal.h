@@ -1,0 +1,53 @@
+// Internal declarations shared by the pgpb translation units.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "pgpb.h"
+
+namespace pgpb {
+
+// Thread-local last-error message (pgpb_last_error).
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+// Device view of a compiled table.  All arrays live in one cudaMalloc arena;
+// every sub-array starts on a 256-byte boundary, so int4/float4 loads are
+// aligned.  Layout rationale: DESIGN.md §3.
+struct TableView {
+  int32_t num_states;
+  int32_t vocab_size;
+  int32_t vocab_padded;        // V rounded up to a multiple of 4
+  int32_t num_arcs;
+  float unk_score;
+  float max_root_score;
+  const float *root_scores;    // [Vp] f32: unk background, root arcs on top (table.py:74-81)
+  const int32_t *root_next;    // [Vp]
+  const int4 *state_rec;       // [S] {arc_start, arc_end, backoff_to, bits(backoff_weight)}
+  const int4 *arcs;            // [A] {token, to, bits(weight), 0}, sorted by (from, token)
+  const int4 *clo_rec;         // [S] {clo_start, clo_count, bits(acc_total), is_final}
+  const int4 *clo;             // [C] {token, next, bits(score), 0}: flattened first-hit arcs
+  const float *final_score;    // [S]
+};
+
+}  // namespace pgpb
+
+struct pgpb_table {
+  pgpb::TableView view;
+  void *arena = nullptr;
+  int64_t arena_bytes = 0;
+  int32_t device = 0;
+  int32_t max_chain = 0;
+  int64_t closure_entries = 0;
+  int32_t max_closure = 0;
+};
+
+#define PGPB_CUDA_TRY(expr)                                                           \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return ::pgpb::fail(PGPB_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)

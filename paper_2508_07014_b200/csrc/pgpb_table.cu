@@ -1,0 +1,203 @@
+// Device-resident compiled table: validation, flattened backoff closure and
+// the packed HBM layout.
+//
+// The reference resolves a cell by walking the failure chain of the query
+// state (_kernels.pyx:56-71).  Chains are short but every level is a
+// dependent load, so besides the packed chain arrays we precompute, once per
+// table, each state's *closure*: the first-hit arcs along its whole chain
+// with their fp32 scores accumulated exactly as the reference does
+// (acc = acc + backoff_weight[s], in chain order) plus the final acc.  One
+// (record, entries) load pair then resolves any state.
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pgpb_internal.h"
+
+namespace {
+
+inline int32_t f2i(float f) {
+  int32_t i;
+  std::memcpy(&i, &f, 4);
+  return i;
+}
+
+inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+}  // namespace
+
+extern "C" {
+
+int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
+                      const int32_t *arc_to, const float *arc_weight,
+                      const int32_t *state_start, const int32_t *state_end,
+                      const int32_t *backoff_to, const float *backoff_weight,
+                      const uint8_t *is_final, const float *final_score, float unk_score,
+                      int32_t device, pgpb_table **out) {
+  using pgpb::fail;
+  if (!out) return fail(PGPB_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (S < 1 || V < 1) return fail(PGPB_EFORMAT, "need at least 1 state and 1 token");
+  if (A < 0) return fail(PGPB_EFORMAT, "negative arc count");
+  // Structural checks the kernels rely on (subset of table.py:87-127).
+  for (int32_t s = 0; s < S; ++s) {
+    if (state_start[s] < 0 || state_start[s] > state_end[s] || state_end[s] > A)
+      return fail(PGPB_EFORMAT, "state " + std::to_string(s) + ": bad arc range");
+    if (backoff_to[s] < 0 || backoff_to[s] >= S)
+      return fail(PGPB_EFORMAT, "backoff_to out of range");
+  }
+  for (int32_t j = 0; j < A; ++j) {
+    if (arc_token[j] < 0 || arc_token[j] >= V) return fail(PGPB_EFORMAT, "arc_token out of range");
+    if (arc_to[j] < 0 || arc_to[j] >= S) return fail(PGPB_EFORMAT, "arc_to out of range");
+  }
+  if (backoff_to[0] != 0) return fail(PGPB_EFORMAT, "root backoff must be (0, 0)");
+
+  const int32_t Vp = (V + 3) & ~3;
+  // Dense root row (table.py:74-81).
+  std::vector<float> root_scores(static_cast<size_t>(Vp), unk_score);
+  std::vector<int32_t> root_next(static_cast<size_t>(Vp), 0);
+  for (int32_t j = state_start[0]; j < state_end[0]; ++j) {
+    root_scores[arc_token[j]] = arc_weight[j];
+    root_next[arc_token[j]] = arc_to[j];
+  }
+  float max_root = root_scores[0];
+  for (int32_t v = 1; v < V; ++v) max_root = std::max(max_root, root_scores[v]);
+
+  std::vector<int4> state_rec(static_cast<size_t>(S));
+  for (int32_t s = 0; s < S; ++s)
+    state_rec[s] = make_int4(state_start[s], state_end[s], backoff_to[s], f2i(backoff_weight[s]));
+  std::vector<int4> arcs(static_cast<size_t>(std::max(A, 1)));
+  for (int32_t j = 0; j < A; ++j) arcs[j] = make_int4(arc_token[j], arc_to[j], f2i(arc_weight[j]), 0);
+
+  // Flattened closure, R5 of SURVEY appendix / _kernels.pyx:56-67:
+  // walk the chain, first hit per token wins, fp32 acc in chain order.
+  std::vector<int4> clo_rec(static_cast<size_t>(S));
+  std::vector<int4> clo;
+  clo.reserve(static_cast<size_t>(A) * 3 + 16);
+  std::vector<int32_t> stamp(static_cast<size_t>(V), -1);
+  std::vector<int4> tmp;
+  int32_t max_chain = 0, max_clo = 0;
+  for (int32_t s0 = 0; s0 < S; ++s0) {
+    tmp.clear();
+    float acc = 0.0f;
+    int32_t s = s0, steps = 0;
+    while (s != 0) {
+      if (++steps > S) return fail(PGPB_EFORMAT, "backoff chain does not reach the root");
+      for (int32_t j = state_start[s]; j < state_end[s]; ++j) {
+        const int32_t v = arc_token[j];
+        if (stamp[v] != s0) {
+          stamp[v] = s0;
+          const float sc = acc + arc_weight[j];
+          tmp.push_back(make_int4(v, arc_to[j], f2i(sc), 0));
+        }
+      }
+      acc = acc + backoff_weight[s];
+      s = backoff_to[s];
+    }
+    std::sort(tmp.begin(), tmp.end(), [](const int4 &a, const int4 &b) { return a.x < b.x; });
+    max_chain = std::max(max_chain, steps);
+    max_clo = std::max(max_clo, static_cast<int32_t>(tmp.size()));
+    if (clo.size() + tmp.size() > static_cast<size_t>(INT32_MAX))
+      return fail(PGPB_ENOMEM, "closure exceeds 2^31 entries");
+    clo_rec[s0] = make_int4(static_cast<int32_t>(clo.size()), static_cast<int32_t>(tmp.size()),
+                            f2i(acc), is_final ? static_cast<int32_t>(is_final[s0] != 0) : 0);
+    clo.insert(clo.end(), tmp.begin(), tmp.end());
+  }
+  const int64_t C = static_cast<int64_t>(clo.size());
+  if (clo.empty()) clo.push_back(make_int4(0, 0, 0, 0));
+
+  std::vector<float> fscore(static_cast<size_t>(S), 0.0f);
+  if (final_score) std::copy(final_score, final_score + S, fscore.begin());
+
+  // One arena, 256-byte aligned sub-arrays.
+  int64_t off = 0;
+  auto place = [&](int64_t bytes) {
+    int64_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  const int64_t o_rs = place(int64_t(Vp) * 4), o_rn = place(int64_t(Vp) * 4);
+  const int64_t o_sr = place(int64_t(S) * 16), o_arc = place(int64_t(arcs.size()) * 16);
+  const int64_t o_cr = place(int64_t(S) * 16), o_clo = place(int64_t(clo.size()) * 16);
+  const int64_t o_fs = place(int64_t(S) * 4);
+  const int64_t total = off;
+
+  int prev_dev = 0;
+  PGPB_CUDA_TRY(cudaGetDevice(&prev_dev));
+  PGPB_CUDA_TRY(cudaSetDevice(device));
+  char *arena = nullptr;
+  cudaError_t e = cudaMalloc(&arena, static_cast<size_t>(total));
+  if (e != cudaSuccess) {
+    cudaSetDevice(prev_dev);
+    return fail(PGPB_ENOMEM, std::string("cudaMalloc(table): ") + cudaGetErrorString(e));
+  }
+  std::vector<char> staging(static_cast<size_t>(total), 0);
+  std::memcpy(staging.data() + o_rs, root_scores.data(), size_t(Vp) * 4);
+  std::memcpy(staging.data() + o_rn, root_next.data(), size_t(Vp) * 4);
+  std::memcpy(staging.data() + o_sr, state_rec.data(), size_t(S) * 16);
+  std::memcpy(staging.data() + o_arc, arcs.data(), arcs.size() * 16);
+  std::memcpy(staging.data() + o_cr, clo_rec.data(), size_t(S) * 16);
+  std::memcpy(staging.data() + o_clo, clo.data(), clo.size() * 16);
+  std::memcpy(staging.data() + o_fs, fscore.data(), size_t(S) * 4);
+  e = cudaMemcpy(arena, staging.data(), static_cast<size_t>(total), cudaMemcpyHostToDevice);
+  cudaSetDevice(prev_dev);
+  if (e != cudaSuccess) {
+    cudaFree(arena);
+    return fail(PGPB_ECUDA, std::string("cudaMemcpy(table): ") + cudaGetErrorString(e));
+  }
+
+  auto *t = new pgpb_table();
+  t->arena = arena;
+  t->arena_bytes = total;
+  t->device = device;
+  t->max_chain = max_chain;
+  t->closure_entries = C;
+  t->max_closure = max_clo;
+  pgpb::TableView &v = t->view;
+  v.num_states = S;
+  v.vocab_size = V;
+  v.vocab_padded = Vp;
+  v.num_arcs = A;
+  v.unk_score = unk_score;
+  v.max_root_score = max_root;
+  v.root_scores = reinterpret_cast<const float *>(arena + o_rs);
+  v.root_next = reinterpret_cast<const int32_t *>(arena + o_rn);
+  v.state_rec = reinterpret_cast<const int4 *>(arena + o_sr);
+  v.arcs = reinterpret_cast<const int4 *>(arena + o_arc);
+  v.clo_rec = reinterpret_cast<const int4 *>(arena + o_cr);
+  v.clo = reinterpret_cast<const int4 *>(arena + o_clo);
+  v.final_score = reinterpret_cast<const float *>(arena + o_fs);
+  *out = t;
+  return PGPB_OK;
+}
+
+int pgpb_table_info_get(const pgpb_table *t, pgpb_table_info *out) {
+  if (!t || !out) return pgpb::fail(PGPB_EINVAL, "NULL argument");
+  out->num_states = t->view.num_states;
+  out->vocab_size = t->view.vocab_size;
+  out->num_arcs = t->view.num_arcs;
+  out->max_chain = t->max_chain;
+  out->closure_entries = t->closure_entries;
+  out->max_closure = t->max_closure;
+  out->device = t->device;
+  out->device_bytes = t->arena_bytes;
+  out->unk_score = t->view.unk_score;
+  out->max_root_score = t->view.max_root_score;
+  return PGPB_OK;
+}
+
+void pgpb_table_destroy(pgpb_table *t) {
+  if (!t) return;
+  if (t->arena) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(t->device);
+    cudaFree(t->arena);
+    cudaSetDevice(prev);
+  }
+  delete t;
+}
+
+}  // extern "C"
