@@ -1,13 +1,15 @@
 // Advance kernel: scores[B,V], next[B,V] for a batch of tree states.
 //
 // Reference: _kernels.score_batch (_kernels.pyx:30-72), R5 in SURVEY.md.
-// HBM-write-bound (8 B written per cell).  One warp per row,
-// rows grid-strided over a persistent grid; the dense root row is staged in
-// shared memory once per CTA; every row is written with 16-byte streaming
-// stores (st.global.cs.v4) shifted by the state's accumulated backoff, then
-// the state's flattened first-hit arcs are scattered on top.  __syncwarp()
-// orders the scatter after the dense stores of the same warp.
+// HBM-write-bound (8 B written per cell).  The production
+// kernel is advance_v5_kernel (single-pass full-line stores, ~80% of the
+// measured HBM copy bandwidth at 8192 x 1024, profiles/); v1 (warp per row,
+// dense stores then scattered overrides), v2 (chunked CTAs), v3 (TMA bulk
+// stores from shared memory) and the chain-walk kernel are kept selectable
+// through PGPB_ADVANCE_VARIANT for measurement and as cross-checks.
 
+#include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "pgpb_common.cuh"
@@ -164,6 +166,239 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// v2: chunked persistent CTAs.  Each CTA owns a contiguous run of rows; its
+// prologue loads every row's state and closure record into shared memory
+// (overlapping the root-row staging), and each warp prefetches its row's
+// closure entries before issuing the dense stores, so the dependent-load
+// latency hides behind the store stream.
+template <bool kVec, bool kSmemRoot>
+__global__ void __launch_bounds__(kThreads, 4)
+    advance_v2_kernel(TableView t, const int32_t *__restrict__ states, int64_t B,
+                      float *__restrict__ scores, int32_t *__restrict__ next, int rows_per_cta) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t r0 = int64_t(blockIdx.x) * rows_per_cta;
+  const int n = static_cast<int>(min(int64_t(rows_per_cta), B - r0));
+  int4 *s_rec = reinterpret_cast<int4 *>(smem);
+  const size_t rec_bytes = (size_t(rows_per_cta) * 16 + 255) & ~size_t(255);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_rec[i] = __ldg(t.clo_rec + __ldg(states + r0 + i));
+  const float *root = t.root_scores;
+  const int32_t *rnext = t.root_next;
+  if (kSmemRoot) {
+    float *s_root = reinterpret_cast<float *>(smem + rec_bytes);
+    int32_t *s_next = reinterpret_cast<int32_t *>(smem + rec_bytes + size_t(t.vocab_padded) * 4);
+    stage_root(t, s_root, s_next);
+    root = s_root;
+    rnext = s_next;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int V = t.vocab_size;
+  for (int j = threadIdx.x >> 5; j < n; j += kWarpsPerBlock) {
+    const int4 rec = s_rec[j];
+    int4 e0 = make_int4(0, 0, 0, 0);
+    if (lane < rec.y) e0 = __ldg(t.clo + rec.x + lane);
+    const int64_t row = r0 + j;
+    float *srow = scores + row * V;
+    int32_t *nrow = next + row * V;
+    write_dense_row<kVec>(srow, nrow, root, rnext, __int_as_float(rec.z), V, lane);
+    __syncwarp();
+    if (lane < rec.y) {
+      srow[e0.x] = __int_as_float(e0.z);
+      nrow[e0.x] = e0.y;
+    }
+    for (int i = lane + 32; i < rec.y; i += 32) {
+      const int4 e = __ldg(t.clo + rec.x + i);
+      srow[e.x] = __int_as_float(e.z);
+      nrow[e.x] = e.y;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// v3: rows assembled in shared memory and written by the TMA engine with
+// bulk async copies (cp.async.bulk.global.shared::cta, SASS UBLKCP), double
+// buffered per warp.  Requires V % 4 == 0 (16-byte aligned rows).
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(ssrc));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads)
+    advance_v3_kernel(TableView t, const int32_t *__restrict__ states, int64_t B,
+                      float *__restrict__ scores, int32_t *__restrict__ next, int warps) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int V = t.vocab_size;
+  const int Vp = t.vocab_padded;
+  float *s_root = reinterpret_cast<float *>(smem);
+  int32_t *s_next = reinterpret_cast<int32_t *>(smem + size_t(Vp) * 4);
+  stage_root(t, s_root, s_next);
+  __syncthreads();
+  const int wib = threadIdx.x >> 5;
+  if (wib >= warps) return;
+  const int lane = threadIdx.x & 31;
+  // per-warp double buffer: [2][scores Vp | next Vp]
+  unsigned char *wbuf = smem + size_t(Vp) * 8 + size_t(wib) * 2 * size_t(Vp) * 8;
+  const int64_t nw = int64_t(gridDim.x) * warps;
+  const int V4 = V >> 2;
+  const float4 *r4 = reinterpret_cast<const float4 *>(s_root);
+  const int4 *q4 = reinterpret_cast<const int4 *>(s_next);
+  int buf = 0;
+  int64_t row = int64_t(blockIdx.x) * warps + wib;
+  int4 rec = make_int4(0, 0, 0, 0);
+  if (row < B) rec = __ldg(t.clo_rec + __ldg(states + row));
+  for (; row < B; row += nw) {
+    // prefetch the next row's record and this row's first closure entries
+    int4 nrec = make_int4(0, 0, 0, 0);
+    if (row + nw < B) nrec = __ldg(t.clo_rec + __ldg(states + row + nw));
+    int4 e0 = make_int4(0, 0, 0, 0);
+    if (lane < rec.y) e0 = __ldg(t.clo + rec.x + lane);
+    float *sb = reinterpret_cast<float *>(wbuf + size_t(buf) * Vp * 8);
+    int32_t *nb = reinterpret_cast<int32_t *>(sb + Vp);
+    // the bulk store issued two rows ago from this buffer must have
+    // finished reading it
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    const float acc = __int_as_float(rec.z);
+    float4 *sb4 = reinterpret_cast<float4 *>(sb);
+    int4 *nb4 = reinterpret_cast<int4 *>(nb);
+#pragma unroll 4
+    for (int i = lane; i < V4; i += 32) {
+      float4 r = r4[i];
+      r.x = acc + r.x;
+      r.y = acc + r.y;
+      r.z = acc + r.z;
+      r.w = acc + r.w;
+      sb4[i] = r;
+      nb4[i] = q4[i];
+    }
+    __syncwarp();
+    if (lane < rec.y) {
+      sb[e0.x] = __int_as_float(e0.z);
+      nb[e0.x] = e0.y;
+    }
+    for (int i = lane + 32; i < rec.y; i += 32) {
+      const int4 e = __ldg(t.clo + rec.x + i);
+      sb[e.x] = __int_as_float(e.z);
+      nb[e.x] = e.y;
+    }
+    fence_async_shared();
+    __syncwarp();
+    if (lane == 0) {
+      bulk_store(scores + row * V, sb, uint32_t(V) * 4);
+      bulk_store(next + row * V, nb, uint32_t(V) * 4);
+      bulk_commit();
+    }
+    buf ^= 1;
+    rec = nrec;
+  }
+  if (lane == 0) bulk_wait_read<0>();
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// v5: single-pass full-line stores.  A row's closure overrides are first
+// dropped into a per-warp shared scratch row + bitmap; the dense pass then
+// merges them into the 16-byte vectors in registers, so every output byte is
+// written exactly once with st.global.cs.v4 (no partial-sector rewrites).
+// The next row's closure entries are prefetched into registers while the
+// current row streams out.  Requires V % 4 == 0 and smem root staging.
+__global__ void __launch_bounds__(kThreads, 3)
+    advance_v5_kernel(TableView t, const int32_t *__restrict__ states, int64_t B,
+                      float *__restrict__ scores, int32_t *__restrict__ next, int rows_per_cta) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int V = t.vocab_size, Vp = t.vocab_padded, Vw = (V + 31) >> 5;
+  const int64_t r0 = int64_t(blockIdx.x) * rows_per_cta;
+  const int n = static_cast<int>(min(int64_t(rows_per_cta), B - r0));
+  const size_t rec_bytes = (size_t(rows_per_cta) * 16 + 255) & ~size_t(255);
+  int4 *s_rec = reinterpret_cast<int4 *>(smem);
+  float *s_root = reinterpret_cast<float *>(smem + rec_bytes);
+  int32_t *s_next = reinterpret_cast<int32_t *>(smem + rec_bytes + size_t(Vp) * 4);
+  const size_t wbytes = size_t(Vp) * 8 + ((size_t(Vw) * 4 + 15) & ~size_t(15));
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *wb = smem + rec_bytes + size_t(Vp) * 8 + size_t(wib) * wbytes;
+  float *ovs = reinterpret_cast<float *>(wb);
+  int32_t *ovn = reinterpret_cast<int32_t *>(wb + size_t(Vp) * 4);
+  unsigned *bm = reinterpret_cast<unsigned *>(wb + size_t(Vp) * 8);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_rec[i] = __ldg(t.clo_rec + __ldg(states + r0 + i));
+  stage_root(t, s_root, s_next);
+  for (int w = lane; w < Vw; w += 32) bm[w] = 0u;
+  __syncthreads();
+  const float4 *r4 = reinterpret_cast<const float4 *>(s_root);
+  const int4 *q4 = reinterpret_cast<const int4 *>(s_next);
+  const int V4 = V >> 2;
+  int j = wib;
+  int4 rec = j < n ? s_rec[j] : make_int4(0, 0, 0, 0);
+  int4 e = (lane < rec.y) ? __ldg(t.clo + rec.x + lane) : make_int4(0, 0, 0, 0);
+  const int W = blockDim.x >> 5;
+  for (; j < n; j += W) {
+    // overrides of this row -> scratch + bitmap
+    if (lane < rec.y) {
+      ovs[e.x] = __int_as_float(e.z);
+      ovn[e.x] = e.y;
+      atomicOr(bm + (e.x >> 5), 1u << (e.x & 31));
+    }
+    for (int i = lane + 32; i < rec.y; i += 32) {
+      const int4 e2 = __ldg(t.clo + rec.x + i);
+      ovs[e2.x] = __int_as_float(e2.z);
+      ovn[e2.x] = e2.y;
+      atomicOr(bm + (e2.x >> 5), 1u << (e2.x & 31));
+    }
+    // prefetch the next row's record and first closure entries
+    const int jn = j + W;
+    const int4 nrec = jn < n ? s_rec[jn] : make_int4(0, 0, 0, 0);
+    const int4 ne = (lane < nrec.y) ? __ldg(t.clo + nrec.x + lane) : make_int4(0, 0, 0, 0);
+    __syncwarp();
+    const float acc = __int_as_float(rec.z);
+    const int64_t row = r0 + j;
+    float4 *s4 = reinterpret_cast<float4 *>(scores + row * V);
+    int4 *n4 = reinterpret_cast<int4 *>(next + row * V);
+#pragma unroll 4
+    for (int c = lane; c < V4; c += 32) {
+      float4 r = r4[c];
+      int4 q = q4[c];
+      r.x = acc + r.x;
+      r.y = acc + r.y;
+      r.z = acc + r.z;
+      r.w = acc + r.w;
+      const unsigned bits = (bm[c >> 3] >> ((c & 7) * 4)) & 0xFu;
+      if (bits) {
+        const int v = 4 * c;
+        if (bits & 1u) { r.x = ovs[v]; q.x = ovn[v]; }
+        if (bits & 2u) { r.y = ovs[v + 1]; q.y = ovn[v + 1]; }
+        if (bits & 4u) { r.z = ovs[v + 2]; q.z = ovn[v + 2]; }
+        if (bits & 8u) { r.w = ovs[v + 3]; q.w = ovn[v + 3]; }
+      }
+      __stcs(s4 + c, r);
+      __stcs(n4 + c, q);
+    }
+    __syncwarp();
+    for (int w = lane; w < Vw; w += 32) bm[w] = 0u;
+    __syncwarp();
+    rec = nrec;
+    e = ne;
+  }
+}
+
+static int g_variant = -1;
+
+static int advance_variant() {
+  if (g_variant < 0) {
+    const char *e = getenv("PGPB_ADVANCE_VARIANT");
+    g_variant = e ? atoi(e) : 5;
+  }
+  return g_variant;
+}
+
 using AdvFn = void (*)(TableView, const int32_t *, int64_t, float *, int32_t *);
 
 static int launch_advance(const pgpb_table *table, const int32_t *d_states, int64_t B,
@@ -177,6 +412,72 @@ static int launch_advance(const pgpb_table *table, const int32_t *d_states, int6
                    (reinterpret_cast<uintptr_t>(d_next) % 16) == 0;
   const size_t root_bytes = size_t(t.vocab_padded) * 8;
   const bool smem_root = root_bytes <= size_t(kMaxSmemRootBytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nsm = sm_count(current_device());
+  const int variant = chain ? 1 : advance_variant();
+  if (variant == 5 && vec && smem_root) {
+    const int Vw = (t.vocab_size + 31) >> 5;
+    const size_t wbytes = size_t(t.vocab_padded) * 8 + ((size_t(Vw) * 4 + 15) & ~size_t(15));
+    const char *e = getenv("PGPB_V5_CTAS");
+    int per_sm = e ? atoi(e) : 3;
+    int W = kWarpsPerBlock;
+    for (;;) {
+      int64_t ctas = int64_t(nsm) * per_sm;
+      int rows = int((B + ctas - 1) / ctas);
+      if (rows < 1) rows = 1;
+      ctas = (B + rows - 1) / rows;
+      const size_t rec_bytes = (size_t(rows) * 16 + 255) & ~size_t(255);
+      const size_t smem5 = rec_bytes + root_bytes + size_t(W) * wbytes;
+      if (smem5 * per_sm <= 224 * 1024 || (per_sm == 1 && smem5 <= 224 * 1024)) {
+        PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(advance_v5_kernel),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem5)));
+        advance_v5_kernel<<<unsigned(ctas), 32 * W, smem5, st>>>(t, d_states, B, d_scores, d_next, rows);
+        PGPB_CUDA_TRY(cudaGetLastError());
+        return PGPB_OK;
+      }
+      if (per_sm > 1) --per_sm;
+      else if (W > 1) --W;
+      else break;
+    }
+  }
+  if (variant == 3 && vec) {
+    // warps per CTA limited by the per-warp double buffer (2 rows of V*8 B)
+    const size_t per_warp = 2 * root_bytes;
+    int warps = int((200 * 1024 - root_bytes) / per_warp);
+    if (const char *e = getenv("PGPB_V3_WARPS")) warps = std::min(warps, atoi(e));
+    warps = warps < 1 ? 1 : (warps > kWarpsPerBlock ? kWarpsPerBlock : warps);
+    const size_t smem3 = root_bytes + size_t(warps) * per_warp;
+    if (smem3 <= 227 * 1024) {
+      PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(advance_v3_kernel),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem3)));
+      int64_t g = (B + warps - 1) / warps;
+      const int per_sm3 = std::max(1, int((227 * 1024) / (smem3 + 1024)));
+      if (g > int64_t(nsm) * per_sm3) g = int64_t(nsm) * per_sm3;
+      advance_v3_kernel<<<unsigned(g), kThreads, smem3, st>>>(t, d_states, B, d_scores, d_next, warps);
+      PGPB_CUDA_TRY(cudaGetLastError());
+      return PGPB_OK;
+    }
+  }
+  if (variant >= 2) {
+    // v2: ~4 resident CTAs per SM, contiguous row chunks
+    int64_t ctas = int64_t(nsm) * 4;
+    int rows = int((B + ctas - 1) / ctas);
+    if (rows < 1) rows = 1;
+    ctas = (B + rows - 1) / rows;
+    const size_t rec_bytes = (size_t(rows) * 16 + 255) & ~size_t(255);
+    const size_t smem2 = rec_bytes + (smem_root ? root_bytes : 0);
+    if (smem2 <= 200 * 1024) {
+      auto fn2 = vec ? (smem_root ? advance_v2_kernel<true, true> : advance_v2_kernel<true, false>)
+                     : (smem_root ? advance_v2_kernel<false, true> : advance_v2_kernel<false, false>);
+      if (smem2 > 48 * 1024) {
+        PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn2),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+      }
+      fn2<<<unsigned(ctas), kThreads, smem2, st>>>(t, d_states, B, d_scores, d_next, rows);
+      PGPB_CUDA_TRY(cudaGetLastError());
+      return PGPB_OK;
+    }
+  }
   const size_t smem = smem_root ? root_bytes : 0;
   AdvFn fn;
   if (chain) {

@@ -31,6 +31,14 @@ struct TableView {
   const int4 *clo_rec;         // [S] {clo_start, clo_count, bits(acc_total), is_final}
   const int4 *clo;             // [C] {token, next, bits(score), 0}: flattened first-hit arcs
   const float *final_score;    // [S]
+  // Linked-automaton layout for the sequential decoders: per state s, at
+  // blob[blob_off[s]] a header {count, bits(acc_total), s, 0} followed by
+  // its `count` closure entries {token, next, bits(score), blob_off[next]},
+  // so a decoder that knows the blob offset of its current state resolves
+  // it with one contiguous load and carries the successor's offset along.
+  const int4 *blob;            // [S + C]
+  const int32_t *blob_off;     // [S]
+  const int32_t *root_next_off;  // [Vp] blob_off[root_next[v]]
 };
 
 }  // namespace pgpb

@@ -108,6 +108,30 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   const int64_t C = static_cast<int64_t>(clo.size());
   if (clo.empty()) clo.push_back(make_int4(0, 0, 0, 0));
 
+  // Blob layout (pgpb_internal.h): header + entries per state, entries carry
+  // the successor's blob offset.
+  std::vector<int32_t> boff(static_cast<size_t>(S));
+  {
+    int64_t o = 0;
+    for (int32_t s0 = 0; s0 < S; ++s0) {
+      boff[s0] = static_cast<int32_t>(o);
+      o += 1 + clo_rec[s0].y;
+    }
+    if (o > INT32_MAX) return fail(PGPB_ENOMEM, "blob exceeds 2^31 entries");
+  }
+  std::vector<int4> blob(static_cast<size_t>(S) + static_cast<size_t>(C));
+  for (int32_t s0 = 0; s0 < S; ++s0) {
+    const int4 r = clo_rec[s0];
+    int4 *b = blob.data() + boff[s0];
+    b[0] = make_int4(r.y, r.z, s0, 0);
+    for (int32_t i = 0; i < r.y; ++i) {
+      const int4 e = clo[static_cast<size_t>(r.x) + i];
+      b[1 + i] = make_int4(e.x, e.y, e.z, boff[e.y]);
+    }
+  }
+  std::vector<int32_t> rn_off(static_cast<size_t>(Vp), 0);
+  for (int32_t v = 0; v < Vp; ++v) rn_off[v] = boff[root_next[v]];
+
   std::vector<float> fscore(static_cast<size_t>(S), 0.0f);
   if (final_score) std::copy(final_score, final_score + S, fscore.begin());
 
@@ -122,6 +146,9 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   const int64_t o_sr = place(int64_t(S) * 16), o_arc = place(int64_t(arcs.size()) * 16);
   const int64_t o_cr = place(int64_t(S) * 16), o_clo = place(int64_t(clo.size()) * 16);
   const int64_t o_fs = place(int64_t(S) * 4);
+  const int64_t o_blob = place(int64_t(blob.size()) * 16);
+  const int64_t o_boff = place(int64_t(S) * 4);
+  const int64_t o_rno = place(int64_t(Vp) * 4);
   const int64_t total = off;
 
   int prev_dev = 0;
@@ -141,6 +168,9 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   std::memcpy(staging.data() + o_cr, clo_rec.data(), size_t(S) * 16);
   std::memcpy(staging.data() + o_clo, clo.data(), clo.size() * 16);
   std::memcpy(staging.data() + o_fs, fscore.data(), size_t(S) * 4);
+  std::memcpy(staging.data() + o_blob, blob.data(), blob.size() * 16);
+  std::memcpy(staging.data() + o_boff, boff.data(), size_t(S) * 4);
+  std::memcpy(staging.data() + o_rno, rn_off.data(), size_t(Vp) * 4);
   e = cudaMemcpy(arena, staging.data(), static_cast<size_t>(total), cudaMemcpyHostToDevice);
   cudaSetDevice(prev_dev);
   if (e != cudaSuccess) {
@@ -169,6 +199,9 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   v.clo_rec = reinterpret_cast<const int4 *>(arena + o_cr);
   v.clo = reinterpret_cast<const int4 *>(arena + o_clo);
   v.final_score = reinterpret_cast<const float *>(arena + o_fs);
+  v.blob = reinterpret_cast<const int4 *>(arena + o_blob);
+  v.blob_off = reinterpret_cast<const int32_t *>(arena + o_boff);
+  v.root_next_off = reinterpret_cast<const int32_t *>(arena + o_rno);
   *out = t;
   return PGPB_OK;
 }

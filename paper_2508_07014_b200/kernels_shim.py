@@ -59,6 +59,7 @@ class _ShimTable:
             _lib.ptr(state_end), _lib.ptr(backoff_to), _lib.ptr(backoff_weight), _lib.ptr(fin), _lib.ptr(fs),
             unk, _current_device(), _lib.ctypes.byref(h)), "pgpb_table_create")
         self.handle = h.value
+        self._destroy = _lib.LIB.pgpb_table_destroy
         # the device table derives its root row from the arcs + unk score
         # (table.py:74-81); refuse a caller-supplied row that differs
         exp_s = np.full(V, np.float32(unk), np.float32)
@@ -70,8 +71,8 @@ class _ShimTable:
             raise ValueError("root row inconsistent with the arc table")
 
     def __del__(self):
-        if getattr(self, "handle", None):
-            _lib.LIB.pgpb_table_destroy(self.handle)
+        if getattr(self, "handle", None) and getattr(self, "_destroy", None) is not None:
+            self._destroy(self.handle)
 
 
 def _current_device() -> int:

@@ -55,6 +55,7 @@ class _DeviceTable:
         self.device = device
         self._keep = None
         self._row_max = None
+        self._destroy = _lib.LIB.pgpb_table_destroy  # survives interpreter teardown
 
     def info(self) -> _lib.TableInfo:
         out = _lib.TableInfo()
@@ -73,8 +74,8 @@ class _DeviceTable:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h:
-            _lib.LIB.pgpb_table_destroy(h)
+        if h and getattr(self, "_destroy", None) is not None:
+            self._destroy(h)
             self.handle = None
 
 
@@ -255,14 +256,26 @@ def get_scores_batch(table: ArcTable, states, *, check: bool = True, out=None) -
     if st.size and (st.min() < 0 or st.max() >= table.num_states):
         raise IndexError(f"state id out of range [0, {table.num_states})")
     B, V = st.shape[0], table.vocab_size
-    scores = np.empty((B, V), dtype=np.float32)
-    nxt = np.empty((B, V), dtype=np.int32)
+    scores, nxt = _host_out(B, V)
     if B:
         dev = table.device_table()
         _lib.check(_lib.LIB.pgpb_advance_host(
             dev.handle, _lib.ptr(st), B, _lib.ptr(scores), _lib.ptr(nxt), _lib.stream_ptr(),
         ), "pgpb_advance_host")
     return ScoreQueryResult(scores=scores, next_states=nxt)
+
+
+def _host_out(B: int, V: int):
+    """Fresh (B, V) float32 / int32 host outputs in page-locked memory, so the
+    device-to-host copy of the result runs at full link speed.  The arrays
+    are ordinary numpy arrays (they keep their pinned torch storage alive)."""
+    import torch
+
+    if B * V == 0:
+        return np.empty((B, V), np.float32), np.empty((B, V), np.int32)
+    s = torch.empty((B, V), dtype=torch.float32, pin_memory=True)
+    n = torch.empty((B, V), dtype=torch.int32, pin_memory=True)
+    return s.numpy(), n.numpy()
 
 
 def _advance_device(table: ArcTable, states, *, check: bool, out, chain: bool = False) -> ScoreQueryResult:
