@@ -9,6 +9,7 @@ reference's exception types (ValueError / IndexError / TableFormatError).
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_uint8, c_void_p
 from pathlib import Path
 
@@ -16,7 +17,7 @@ import numpy as np
 
 from .errors import TableFormatError
 
-LIB_PATH = Path(__file__).resolve().parent / "libpgpb.so"
+LIB_PATH = Path(os.environ.get("PGPB_LIB_PATH") or Path(__file__).resolve().parent / "libpgpb.so")
 
 PGPB_OK = 0
 PGPB_EINVAL = -1

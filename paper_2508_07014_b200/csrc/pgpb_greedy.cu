@@ -16,42 +16,61 @@
 
 namespace pgpb {
 
+constexpr int kStepTopM = 4;
+
+// One label-looping step: a warp per row makes one pass over the row for
+// its top-M tokens (entry 0 = the argmax), then, for non-blank rows with
+// boosting on, resolves the rerank with blob_rerank (closure arcs exact,
+// dense tokens among the top-M, exact bound, full-row fallback).
 template <bool kVec>
 __global__ void __launch_bounds__(kThreads)
-    greedy_step_kernel(TableView t, int use_boost, int smem_root, const float *__restrict__ lp,
-                       int64_t ld, int64_t R, int V, const int32_t *__restrict__ states,
-                       const uint8_t *__restrict__ active, int blank, double lam,
-                       int32_t *__restrict__ chosen, float *__restrict__ lp_chosen,
+    greedy_step_kernel(TableView t, int use_boost, const float *__restrict__ lp, int64_t ld, int64_t R,
+                       int V, const int32_t *__restrict__ states, const uint8_t *__restrict__ active,
+                       int blank, double lam, int32_t *__restrict__ chosen, float *__restrict__ lp_chosen,
                        double *__restrict__ delta, int32_t *__restrict__ next_state,
                        uint8_t *__restrict__ is_blank) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const float *root;
-  const int32_t *rnext;
-  unsigned *bm;
-  setup_smem(t, use_boost, smem_root, smem, root, rnext, bm);
+  const int Vp = t.vocab_padded, Vw = (V + 31) >> 5;
+  float *s_root = reinterpret_cast<float *>(smem);
+  int32_t *s_rnext = reinterpret_cast<int32_t *>(smem + size_t(Vp) * 4);
+  int32_t *s_rnoff = reinterpret_cast<int32_t *>(smem + size_t(Vp) * 8);
+  unsigned *bm = reinterpret_cast<unsigned *>(smem + size_t(Vp) * 12) + (threadIdx.x >> 5) * Vw;
   const int lane = threadIdx.x & 31;
+  if (use_boost) {
+    for (int i = threadIdx.x; i < Vp; i += blockDim.x) {
+      s_root[i] = __ldg(t.root_scores + i);
+      s_rnext[i] = __ldg(t.root_next + i);
+      s_rnoff[i] = __ldg(t.root_next_off + i);
+    }
+    for (int i = lane; i < Vw; i += 32) bm[i] = 0u;
+  }
+  __syncthreads();
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
     if (active && !__ldg(active + r)) continue;
     const float *row = lp + r * ld;
-    float best;
-    int a;
-    warp_row_argmax<kVec>(row, V, lane, best, a);
-    RerankOut o;
+    int tv[kStepTopM];
+    float tx[kStepTopM];
+    warp_row_topm<kStepTopM, kVec>(row, V, lane, tv, tx);
+    const int a = tv[0];
     const bool blk = (a == blank);
-    if (blk || !use_boost) {
-      o.chosen = a;
-      o.lp = best;
-      o.delta = 0.0;
-      o.next = 0;
-    } else {
-      o = warp_rerank<kVec>(t, root, rnext, bm, row, V, __ldg(states + r), blank, -1, lam, lane);
+    int c = a, nx = 0;
+    float lpc = tx[0];
+    double d = 0.0;
+    if (!blk && use_boost) {
+      const int soff = __ldg(t.blob_off + __ldg(states + r));
+      const BCand w = blob_rerank<kStepTopM>(t, s_root, s_rnext, s_rnoff, bm, row, V, soff, tv, tx, blank, -1,
+                                             lam, t.max_root_score, lane);
+      c = w.v;
+      lpc = w.lp;
+      d = static_cast<double>(w.s);
+      nx = w.nx;
     }
     if (lane == 0) {
-      chosen[r] = o.chosen;
-      lp_chosen[r] = o.lp;
-      delta[r] = o.delta;
-      next_state[r] = o.next;
+      chosen[r] = c;
+      lp_chosen[r] = lpc;
+      delta[r] = d;
+      next_state[r] = nx;
       is_blank[r] = blk ? 1 : 0;
     }
   }
@@ -101,16 +120,16 @@ int pgpb_greedy_step(const pgpb_table *table, const float *d_lp, int64_t ld, int
                                  std::to_string(table->view.vocab_size));
   if (R == 0) return PGPB_OK;
   const TableView t = table ? table->view : empty_view(V);
-  bool smem_root = false;
-  const size_t smem = greedy_smem(t, use_boost != 0, smem_root);
+  const size_t smem = use_boost ? size_t(t.vocab_padded) * 12 + size_t(kWarpsPerBlock) * ((V + 31) >> 5) * 4 : 0;
+  if (smem > 220 * 1024) return fail(PGPB_EINVAL, "vocabulary too large for the shared-memory root row");
   const bool vec = (V % 4) == 0 && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(d_lp) % 16) == 0;
   auto fn = vec ? greedy_step_kernel<true> : greedy_step_kernel<false>;
   int rc = prep_kernel(fn, smem);
   if (rc) return rc;
   const unsigned grid = warp_grid(R, 4);
   fn<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      t, use_boost ? 1 : 0, smem_root ? 1 : 0, d_lp, ld, R, V, d_states, d_active, blank, lam,
-      d_chosen, d_lp_chosen, d_delta, d_next, d_is_blank);
+      t, use_boost ? 1 : 0, d_lp, ld, R, V, d_states, d_active, blank, lam, d_chosen, d_lp_chosen, d_delta,
+      d_next, d_is_blank);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }

@@ -119,7 +119,8 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
     }
     if (o > INT32_MAX) return fail(PGPB_ENOMEM, "blob exceeds 2^31 entries");
   }
-  std::vector<int4> blob(static_cast<size_t>(S) + static_cast<size_t>(C));
+  // +64 zero entries of padding: warp-wide loads read up to 64 entries past a header
+  std::vector<int4> blob(static_cast<size_t>(S) + static_cast<size_t>(C) + 64, make_int4(0, 0, 0, 0));
   for (int32_t s0 = 0; s0 < S; ++s0) {
     const int4 r = clo_rec[s0];
     int4 *b = blob.data() + boff[s0];
