@@ -269,8 +269,11 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
     }
     if not args.no_decode:
-        out["decode"] = bench_decode(tab, V, dev, rank, world)
-        out["gpu_launches"] += out["decode"].pop("_launches", 0)
+        out["decode_rnnt"] = bench_rnnt(tab, V, dev, rank, world)
+        out["gpu_launches"] += out["decode_rnnt"].pop("_launches", 0)
+        out["boosted_decode_rtfx"] = out["decode_rnnt"]["boosted"]["rtfx"]
+        out["decode_ctc"] = bench_decode(tab, V, dev, rank, world)
+        out["gpu_launches"] += out["decode_ctc"].pop("_launches", 0)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(tab, B, V)
     return out
@@ -324,6 +327,44 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
         del lp
     out["_launches"] = launches
     return out
+
+
+def bench_rnnt(tab, V, dev, rank, world, B=128, T=200, D=512):
+    """Config 2: greedy RNN-T label-looping with GPU-PB, 20K-phrase tree, V=1024,
+    batch 128 x 200 frames of synthetic encoder output, random-init
+    LSTM-640 prediction net + joint; boosted (lam=1) vs unboosted (lam=0).
+    Device time of one whole batch decode (graph replays + done-flag polls)."""
+    import torch
+
+    import paper_2508_07014_b200 as pb
+    from paper_2508_07014_b200.rnnt import LabelLoopingDecoder, RNNTModel
+
+    model = RNNTModel(V, enc_dim=D, pred_dim=640, joint_dim=640, seed=11 + rank, blank_bias=10.5)
+    g = torch.Generator(device=dev)
+    g.manual_seed(4321 + rank)
+    enc_proj = model.project_encoder(torch.randn((B, T, D), generator=g, device=dev))
+    res = {"workload": f"greedy RNN-T label looping, batch {B} x {T} frames, V={V}, 20K-phrase tree, "
+                       "LSTM-640 pred net + joint (random init), lam=1 vs lam=0"}
+    iters = {}
+    for name, cfg in (("unboosted", pb.DecodeConfig(lam=0.0)), ("boosted", pb.DecodeConfig(lam=1.0))):
+        dec = LabelLoopingDecoder(model, tab, cfg, B, T, use_graph=True)
+        dec.decode(enc_proj)  # capture + warm-up
+        times = []
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            o = dec.decode(enc_proj)
+            e.record()
+            torch.cuda.synchronize(dev)
+            times.append(s.elapsed_time(e))
+        ms = statistics.median(times)
+        iters[name] = o.iterations
+        res[name] = {"ms": ms, "rtfx": B * T * FRAME_SEC / (ms / 1e3) * world, "label_iterations": o.iterations,
+                     "emitted_per_utt": float(o.num_out.double().mean().item())}
+    res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
+    res["_launches"] = sum(iters.values()) * 3  # one pgpb_greedy_step per label iteration
+    return res
 
 
 def _ref_module():

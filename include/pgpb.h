@@ -182,6 +182,38 @@ int pgpb_greedy_step(const pgpb_table *table, const float *d_logprobs, int64_t l
                      int32_t *d_chosen, float *d_lp_chosen, double *d_delta,
                      int32_t *d_next_state, uint8_t *d_is_blank, void *stream);
 
+/* Label-looping state of B transducer utterances (all device pointers).
+ * Layout: t, k, lengths, n, last are int64[B]; tree int32[B]; am, boost
+ * float64[B]; tokens/states int32[B, lmax], deltas float64[B, lmax].     */
+typedef struct pgpb_label_loop_state {
+  int64_t *t;        /* current frame                                     */
+  int64_t *k;        /* symbols emitted at the current frame              */
+  const int64_t *lengths;
+  int64_t *n;        /* tokens emitted so far                             */
+  int64_t *last;     /* last emitted token (prediction-net context)       */
+  int32_t *tree;     /* GPU-PB tree state                                 */
+  double *am;
+  double *boost;
+  int32_t *tokens;
+  double *deltas;
+  int32_t *states;
+  int64_t lmax;
+  int32_t cap;       /* max_symbols_per_frame                             */
+} pgpb_label_loop_state;
+
+/* One label-looping iteration fused with its bookkeeping: for every row r
+ * with t[r] < lengths[r], decide the row exactly as pgpb_greedy_step does,
+ * then apply R7 (decoding.py:371-392): blank -> am += lp[blank], next frame;
+ * emission -> am/boost/outputs/tree updated, k += 1, and after `cap`
+ * emissions the frame advances without a blank score.  Writes emit[r]
+ * (1 iff row r emitted) and feed[r] (token the prediction network consumes
+ * next: the emitted token, else last[r]); atomically ORs 1 into *any_active
+ * when some row still has frames left (caller zeroes it).               */
+int pgpb_label_loop_step(const pgpb_table *table, const float *d_logprobs, int64_t ld,
+                         int64_t rows, int32_t vocab_size, int32_t blank, double lam,
+                         int32_t use_boost, const pgpb_label_loop_state *state,
+                         uint8_t *d_emit, int64_t *d_feed, int32_t *d_any_active, void *stream);
+
 /* Per-state maximum of the resolved score row, max_v scores[s, v]
  * (used by the AED eos bump, decoding.py:546-552).  out[S] f32.             */
 int pgpb_row_max(const pgpb_table *table, float *d_out, void *stream);

@@ -42,6 +42,13 @@ class TableInfo(ctypes.Structure):
     ]
 
 
+class LabelLoopState(ctypes.Structure):
+    """pgpb_label_loop_state (include/pgpb.h)."""
+
+    _fields_ = [(n, c_void_p) for n in ("t", "k", "lengths", "n", "last", "tree", "am", "boost", "tokens",
+                                         "deltas", "states")] + [("lmax", c_int64), ("cap", c_int32)]
+
+
 # name -> argtypes (all return int unless listed in _VOID / _OTHER)
 _P = c_void_p
 _SIGS = {
@@ -63,6 +70,8 @@ _SIGS = {
     "pgpb_greedy_step": [c_void_p, _P, c_int64, c_int64, c_int32, _P, _P, c_int32, c_double, c_int32,
                          _P, _P, _P, _P, _P, c_void_p],
     "pgpb_row_max": [c_void_p, _P, c_void_p],
+    "pgpb_label_loop_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32,
+                             POINTER(LabelLoopState), _P, _P, _P, c_void_p],
     "pgpb_beam_topk": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_int32, _P, _P, _P, _P,
                        _P, _P, _P, c_double, c_int32, c_int32, _P, _P, _P, _P, _P, _P, c_void_p],
 }

@@ -24,6 +24,21 @@ int current_device() {
   return d;
 }
 
+// Keep stream-ordered allocations of the *_host entry points cached in the
+// device's default memory pool across synchronizations (the default release
+// threshold of 0 would hand the memory back at every sync and re-map it on
+// the next call).
+void retain_pool(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 int sm_count(int device) {
   if (device < 0 || device >= 64) return 148;
   if (!g_sm_count[device]) {
@@ -527,6 +542,7 @@ int pgpb_advance_host(const pgpb_table *table, const int32_t *h_states, int64_t 
   int prev = 0;
   PGPB_CUDA_TRY(cudaGetDevice(&prev));
   PGPB_CUDA_TRY(cudaSetDevice(table->device));
+  retain_pool(table->device);
   const size_t cells = size_t(B) * size_t(V);
   const size_t o_sc = 0, o_nx = ((cells * 4 + 255) / 256) * 256,
                o_st = o_nx + ((cells * 4 + 255) / 256) * 256;

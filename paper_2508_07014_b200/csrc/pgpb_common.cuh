@@ -16,6 +16,7 @@ constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr int kMaxSmemRootBytes = 160 * 1024;
 
 int sm_count(int device);
+void retain_pool(int device);
 int current_device();
 
 // Grid for a warp-per-item kernel: enough CTAs to cover `items` warps but

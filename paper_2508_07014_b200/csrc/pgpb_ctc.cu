@@ -568,6 +568,7 @@ int pgpb_ctc_greedy(const pgpb_table *table, const float *d_lp, int64_t B, int64
                                  std::to_string(table->view.vocab_size));
   if (B == 0) return PGPB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  retain_pool(current_device());
   const int M = use_boost ? kTopM : 1;
   const int64_t F = B * (T > 0 ? T : 1);
   const size_t idx_bytes = ((size_t(F) * M * 4 + 255) / 256) * 256;
@@ -671,6 +672,7 @@ int pgpb_ctc_greedy_host(const pgpb_table *table, const float *h_lp, int64_t T, 
   using namespace pgpb;
   if (T < 0 || V < 1) return fail(PGPB_EINVAL, "bad shape");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  retain_pool(current_device());
   const size_t lp_bytes = size_t(T) * size_t(V) * 4;
   const size_t Tn = size_t(T > 0 ? T : 1);
   // layout: lp | tokens | states | deltas | am, boost, nout

@@ -18,63 +18,169 @@ namespace pgpb {
 
 constexpr int kStepTopM = 4;
 
-// One label-looping step: a warp per row makes one pass over the row for
-// its top-M tokens (entry 0 = the argmax), then, for non-blank rows with
-// boosting on, resolves the rerank with blob_rerank (closure arcs exact,
-// dense tokens among the top-M, exact bound, full-row fallback).
-template <bool kVec>
-__global__ void __launch_bounds__(kThreads)
-    greedy_step_kernel(TableView t, int use_boost, const float *__restrict__ lp, int64_t ld, int64_t R,
-                       int V, const int32_t *__restrict__ states, const uint8_t *__restrict__ active,
-                       int blank, double lam, int32_t *__restrict__ chosen, float *__restrict__ lp_chosen,
-                       double *__restrict__ delta, int32_t *__restrict__ next_state,
-                       uint8_t *__restrict__ is_blank) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int Vp = t.vocab_padded, Vw = (V + 31) >> 5;
-  float *s_root = reinterpret_cast<float *>(smem);
-  int32_t *s_rnext = reinterpret_cast<int32_t *>(smem + size_t(Vp) * 4);
-  int32_t *s_rnoff = reinterpret_cast<int32_t *>(smem + size_t(Vp) * 8);
-  unsigned *bm = reinterpret_cast<unsigned *>(smem + size_t(Vp) * 12) + (threadIdx.x >> 5) * Vw;
-  const int lane = threadIdx.x & 31;
-  if (use_boost) {
-    for (int i = threadIdx.x; i < Vp; i += blockDim.x) {
-      s_root[i] = __ldg(t.root_scores + i);
-      s_rnext[i] = __ldg(t.root_next + i);
-      s_rnoff[i] = __ldg(t.root_next_off + i);
-    }
-    for (int i = lane; i < Vw; i += 32) bm[i] = 0u;
+// Per-row decision shared by the step and label-loop kernels: one pass over
+// the row for its top-M tokens (entry 0 = the stage-1 argmax); for a
+// non-blank argmax with boosting on, blob_rerank (closure arcs exact, dense
+// tokens among the top-M, exact bound, full-row fallback).  Root-row reads
+// go through L1/L2 (a handful per row), so no shared staging is needed.
+struct RowDecision {
+  int chosen;
+  float lp;
+  double delta;
+  int next;
+  bool blank;
+};
+
+template <int NC>
+__device__ __forceinline__ RowDecision decide_row(const TableView &t, const float *row, int V, int blank, double lam,
+                                                  int use_boost, int state, unsigned *bm, float *sv, int *si,
+                                                  int lane) {
+  int tv[kStepTopM];
+  float tx[kStepTopM];
+  if (NC > 0)
+    warp_row_topm_thr<kStepTopM, (NC > 0 ? NC : 1)>(row, V, lane, sv, si, tv, tx);
+  else
+    warp_row_topm<kStepTopM, false>(row, V, lane, tv, tx);
+  RowDecision d{tv[0], tx[0], 0.0, 0, tv[0] == blank};
+  if (!d.blank && use_boost) {
+    const int soff = __ldg(t.blob_off + state);
+    const BCand w = blob_rerank<kStepTopM>(t, t.root_scores, t.root_next, t.root_next_off, bm, row, V, soff, tv, tx,
+                                           blank, -1, lam, t.max_root_score, lane);
+    d.chosen = w.v;
+    d.lp = w.lp;
+    d.delta = static_cast<double>(w.s);
+    d.next = w.nx;
   }
-  __syncthreads();
+  return d;
+}
+
+struct StepScratch {
+  unsigned *bm;
+  float *sv;
+  int *si;
+};
+
+__device__ __forceinline__ StepScratch step_scratch(unsigned char *smem, int V, int use_boost) {
+  const int Vw = (V + 31) >> 5;
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StepScratch s;
+  s.sv = reinterpret_cast<float *>(smem) + wib * 64;
+  s.si = reinterpret_cast<int *>(s.sv + 32);
+  s.bm = reinterpret_cast<unsigned *>(smem + kWarpsPerBlock * 256) + wib * Vw;
+  if (use_boost)
+    for (int i = lane; i < Vw; i += 32) s.bm[i] = 0u;
+  __syncwarp();
+  return s;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(kThreads)
+    greedy_step_kernel(TableView t, int use_boost, const float *__restrict__ lp, int64_t ld, int64_t R, int V,
+                       const int32_t *__restrict__ states, const uint8_t *__restrict__ active, int blank, double lam,
+                       int32_t *__restrict__ chosen, float *__restrict__ lp_chosen, double *__restrict__ delta,
+                       int32_t *__restrict__ next_state, uint8_t *__restrict__ is_blank) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const StepScratch sc = step_scratch(smem, V, use_boost);
+  const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
     if (active && !__ldg(active + r)) continue;
-    const float *row = lp + r * ld;
-    int tv[kStepTopM];
-    float tx[kStepTopM];
-    warp_row_topm<kStepTopM, kVec>(row, V, lane, tv, tx);
-    const int a = tv[0];
-    const bool blk = (a == blank);
-    int c = a, nx = 0;
-    float lpc = tx[0];
-    double d = 0.0;
-    if (!blk && use_boost) {
-      const int soff = __ldg(t.blob_off + __ldg(states + r));
-      const BCand w = blob_rerank<kStepTopM>(t, s_root, s_rnext, s_rnoff, bm, row, V, soff, tv, tx, blank, -1,
-                                             lam, t.max_root_score, lane);
-      c = w.v;
-      lpc = w.lp;
-      d = static_cast<double>(w.s);
-      nx = w.nx;
-    }
+    const RowDecision d = decide_row<NC>(t, lp + r * ld, V, blank, lam, use_boost,
+                                         use_boost ? __ldg(states + r) : 0, sc.bm, sc.sv, sc.si, lane);
     if (lane == 0) {
-      chosen[r] = c;
-      lp_chosen[r] = lpc;
-      delta[r] = d;
-      next_state[r] = nx;
-      is_blank[r] = blk ? 1 : 0;
+      chosen[r] = d.chosen;
+      lp_chosen[r] = d.lp;
+      delta[r] = d.delta;
+      next_state[r] = d.next;
+      is_blank[r] = d.blank ? 1 : 0;
     }
   }
 }
+
+template <int NC>
+__global__ void __launch_bounds__(kThreads)
+    label_loop_kernel(TableView t, int use_boost, const float *__restrict__ lp, int64_t ld, int64_t R, int V,
+                      int blank, double lam, pgpb_label_loop_state st, uint8_t *__restrict__ emit,
+                      int64_t *__restrict__ feed, int32_t *__restrict__ any_active) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const StepScratch sc = step_scratch(smem, V, use_boost);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
+    const int64_t tr = st.t[r], len = st.lengths[r];
+    if (tr >= len) {  // finished utterance: nothing to decide
+      if (lane == 0) {
+        emit[r] = 0;
+        feed[r] = st.last[r];
+      }
+      continue;
+    }
+    const RowDecision d = decide_row<NC>(t, lp + r * ld, V, blank, lam, use_boost, use_boost ? st.tree[r] : 0,
+                                         sc.bm, sc.sv, sc.si, lane);
+    if (lane == 0) {
+      // R7 bookkeeping (decoding.py:371-392)
+      st.am[r] = st.am[r] + static_cast<double>(d.lp);
+      int64_t tn = tr;
+      if (d.blank) {
+        tn = tr + 1;
+        st.k[r] = 0;
+        emit[r] = 0;
+        feed[r] = st.last[r];
+      } else {
+        const int64_t n = st.n[r];
+        if (n < st.lmax) {
+          st.tokens[r * st.lmax + n] = d.chosen;
+          st.deltas[r * st.lmax + n] = d.delta;
+          st.states[r * st.lmax + n] = d.next;
+        }
+        st.n[r] = n + 1;
+        st.boost[r] = st.boost[r] + d.delta;
+        st.tree[r] = d.next;
+        const int64_t k = st.k[r] + 1;
+        if (k >= st.cap) {  // symbol cap: next frame, no blank score
+          tn = tr + 1;
+          st.k[r] = 0;
+        } else {
+          st.k[r] = k;
+        }
+        st.last[r] = d.chosen;
+        emit[r] = 1;
+        feed[r] = d.chosen;
+      }
+      st.t[r] = tn;
+      if (tn < len) atomicOr(any_active, 1);
+    }
+  }
+}
+
+using StepFn = void (*)(TableView, int, const float *, int64_t, int64_t, int, const int32_t *, const uint8_t *, int,
+                        double, int32_t *, float *, double *, int32_t *, uint8_t *);
+using LoopFn = void (*)(TableView, int, const float *, int64_t, int64_t, int, int, double, pgpb_label_loop_state,
+                        uint8_t *, int64_t *, int32_t *);
+
+// NC = float4 chunks per lane for the register top-M (V <= 1024, 16-byte
+// rows); 0 selects the generic path.
+static int step_nc(int V, int64_t ld, const float *lp) {
+  const bool vec = (V % 4) == 0 && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(lp) % 16) == 0;
+  const int nc = (V + 127) / 128;
+  return (vec && nc <= 8) ? nc : 0;
+}
+
+static StepFn step_fn(int nc) {
+  static const StepFn f[9] = {greedy_step_kernel<0>, greedy_step_kernel<1>, greedy_step_kernel<2>,
+                              greedy_step_kernel<3>, greedy_step_kernel<4>, greedy_step_kernel<5>,
+                              greedy_step_kernel<6>, greedy_step_kernel<7>, greedy_step_kernel<8>};
+  return f[nc];
+}
+
+static LoopFn loop_fn(int nc) {
+  static const LoopFn f[9] = {label_loop_kernel<0>, label_loop_kernel<1>, label_loop_kernel<2>,
+                              label_loop_kernel<3>, label_loop_kernel<4>, label_loop_kernel<5>,
+                              label_loop_kernel<6>, label_loop_kernel<7>, label_loop_kernel<8>};
+  return f[nc];
+}
+
+static size_t step_smem(int V) { return size_t(kWarpsPerBlock) * 256 + size_t(kWarpsPerBlock) * ((V + 31) >> 5) * 4; }
 
 __global__ void __launch_bounds__(kThreads)
     row_max_kernel(TableView t, int smem_root, float *__restrict__ out) {
@@ -120,16 +226,39 @@ int pgpb_greedy_step(const pgpb_table *table, const float *d_lp, int64_t ld, int
                                  std::to_string(table->view.vocab_size));
   if (R == 0) return PGPB_OK;
   const TableView t = table ? table->view : empty_view(V);
-  const size_t smem = use_boost ? size_t(t.vocab_padded) * 12 + size_t(kWarpsPerBlock) * ((V + 31) >> 5) * 4 : 0;
-  if (smem > 220 * 1024) return fail(PGPB_EINVAL, "vocabulary too large for the shared-memory root row");
-  const bool vec = (V % 4) == 0 && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(d_lp) % 16) == 0;
-  auto fn = vec ? greedy_step_kernel<true> : greedy_step_kernel<false>;
+  const size_t smem = step_smem(V);
+  const int nc = step_nc(V, ld, d_lp);
+  StepFn fn = step_fn(nc);
   int rc = prep_kernel(fn, smem);
   if (rc) return rc;
-  const unsigned grid = warp_grid(R, 4);
-  fn<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      t, use_boost ? 1 : 0, d_lp, ld, R, V, d_states, d_active, blank, lam, d_chosen, d_lp_chosen, d_delta,
-      d_next, d_is_blank);
+  const unsigned grid = static_cast<unsigned>((R + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  fn<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(t, use_boost ? 1 : 0, d_lp, ld, R, V, d_states,
+                                                                  d_active, blank, lam, d_chosen, d_lp_chosen,
+                                                                  d_delta, d_next, d_is_blank);
+  PGPB_CUDA_TRY(cudaGetLastError());
+  return PGPB_OK;
+}
+
+int pgpb_label_loop_step(const pgpb_table *table, const float *d_lp, int64_t ld, int64_t R, int32_t V, int32_t blank,
+                         double lam, int32_t use_boost, const pgpb_label_loop_state *state, uint8_t *d_emit,
+                         int64_t *d_feed, int32_t *d_any_active, void *stream) {
+  using namespace pgpb;
+  if (R < 0 || V < 1 || ld < V || !state) return fail(PGPB_EINVAL, "bad shape");
+  if (state->cap < 1) return fail(PGPB_EINVAL, "cap must be >= 1");
+  if (use_boost && !table) return fail(PGPB_EINVAL, "use_boost requires a table");
+  if (table && table->view.vocab_size != V)
+    return fail(PGPB_EINVAL, "step model vocab size " + std::to_string(V) + " != table vocab size " +
+                                 std::to_string(table->view.vocab_size));
+  if (R == 0) return PGPB_OK;
+  const TableView t = table ? table->view : empty_view(V);
+  const size_t smem = step_smem(V);
+  const int nc = step_nc(V, ld, d_lp);
+  LoopFn fn = loop_fn(nc);
+  int rc = prep_kernel(fn, smem);
+  if (rc) return rc;
+  const unsigned grid = static_cast<unsigned>((R + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  fn<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(t, use_boost ? 1 : 0, d_lp, ld, R, V, blank, lam,
+                                                                  *state, d_emit, d_feed, d_any_active);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }

@@ -455,3 +455,129 @@ __device__ __forceinline__ void warp_row_topm(const float *__restrict__ row, int
 }
 
 }  // namespace pgpb
+
+namespace pgpb {
+
+// Top-M of a row held in registers (NC float4 chunks per lane, V <= 128*NC),
+// every lane ends with the same sorted (tv, tx).  Threshold method: the M-th
+// largest lane maximum bounds the row's M-th largest value from below, so
+// only elements >= it (normally exactly M) are ranked; ties producing more
+// than 32 survivors fall back to the insertion network.  `sv`/`si` are 32
+// shared slots private to the warp.
+template <int M, int NC>
+__device__ __forceinline__ void warp_row_topm_thr(const float *__restrict__ row, int V, int lane, float *sv, int *si,
+                                                  int (&tv)[M], float (&tx)[M]) {
+  const float4 *row4 = reinterpret_cast<const float4 *>(row);
+  const int V4 = V >> 2;
+  float4 x[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int c = lane + 32 * k;
+    x[k] = c < V4 ? __ldg(row4 + c) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+  }
+  float lm = -INFINITY;
+  int li = INT_MAX;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int v = 4 * (lane + 32 * k);
+    if (argmax_better(x[k].x, v, lm, li)) { lm = x[k].x; li = v; }
+    if (argmax_better(x[k].y, v + 1, lm, li)) { lm = x[k].y; li = v + 1; }
+    if (argmax_better(x[k].z, v + 2, lm, li)) { lm = x[k].z; li = v + 2; }
+    if (argmax_better(x[k].w, v + 3, lm, li)) { lm = x[k].w; li = v + 3; }
+  }
+  float thr = -INFINITY;
+  {
+    float v = lm;
+    int id = li;
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      float bx = v;
+      int bi = id;
+      warp_argmax(bx, bi);
+      thr = bx;
+      if (r == 0) {
+        tv[0] = bi;
+        tx[0] = bx;
+      }
+      if (id == bi) {
+        v = -INFINITY;
+        id = INT_MAX;
+      }
+    }
+  }
+  if (M == 1) return;
+  int mine = 0;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) mine += (x[k].x >= thr) + (x[k].y >= thr) + (x[k].z >= thr) + (x[k].w >= thr);
+  int pos = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, pos, o);
+    if (lane >= o) pos += y;
+  }
+  const int total = __shfl_sync(kFull, pos, 31);
+  pos -= mine;
+  if (total <= 32) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int v = 4 * (lane + 32 * k);
+      if (x[k].x >= thr) { sv[pos] = x[k].x; si[pos++] = v; }
+      if (x[k].y >= thr) { sv[pos] = x[k].y; si[pos++] = v + 1; }
+      if (x[k].z >= thr) { sv[pos] = x[k].z; si[pos++] = v + 2; }
+      if (x[k].w >= thr) { sv[pos] = x[k].w; si[pos++] = v + 3; }
+    }
+    __syncwarp();
+    float cv = lane < total ? sv[lane] : -INFINITY;
+    int ci = lane < total ? si[lane] : INT_MAX;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      float bx = cv;
+      int bi = ci;
+      warp_argmax(bx, bi);
+      if (ci == bi) {
+        cv = -INFINITY;
+        ci = INT_MAX;
+      }
+      tv[r] = bi;
+      tx[r] = bx;
+    }
+  } else {
+    float lv[M];
+    int lix[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      lv[i] = -INFINITY;
+      lix[i] = INT_MAX;
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const int v = 4 * (lane + 32 * k);
+      if (v < V) {
+        topm_insert<M>(lv, lix, x[k].x, v);
+        topm_insert<M>(lv, lix, x[k].y, v + 1);
+        topm_insert<M>(lv, lix, x[k].z, v + 2);
+        topm_insert<M>(lv, lix, x[k].w, v + 3);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      float bx = lv[0];
+      int bi = lix[0];
+      warp_argmax(bx, bi);
+      if (lix[0] == bi && bi != INT_MAX) {
+#pragma unroll
+        for (int i = 0; i < M - 1; ++i) {
+          lv[i] = lv[i + 1];
+          lix[i] = lix[i + 1];
+        }
+        lv[M - 1] = -INFINITY;
+        lix[M - 1] = INT_MAX;
+      }
+      tv[r] = bi;
+      tx[r] = bx;
+    }
+  }
+}
+
+}  // namespace pgpb
