@@ -542,7 +542,7 @@ int pgpb_advance_host(const pgpb_table *table, const int32_t *h_states, int64_t 
   int prev = 0;
   PGPB_CUDA_TRY(cudaGetDevice(&prev));
   PGPB_CUDA_TRY(cudaSetDevice(table->device));
-  retain_pool(table->device);
+  pgpb::retain_pool(table->device);
   const size_t cells = size_t(B) * size_t(V);
   const size_t o_sc = 0, o_nx = ((cells * 4 + 255) / 256) * 256,
                o_st = o_nx + ((cells * 4 + 255) / 256) * 256;
