@@ -279,6 +279,8 @@ def run_ours(args, rank, world, local):
         out["boosted_decode_rtfx"] = out["decode_rnnt"]["boosted"]["rtfx"]
         out["decode_ctc"] = bench_decode(tab, V, dev, rank, world)
         out["gpu_launches"] += out["decode_ctc"].pop("_launches", 0)
+    if rank == 0 and world == 1 and not args.no_decode:
+        out["decode_beams"] = bench_beams()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(tab, B, V)
     return out
@@ -382,6 +384,73 @@ def bench_rnnt(tab, V, dev, rank, world, B=128, T=200, D=512):
         allres = all_gather_results(local, B * world, with_trace=True)
         res["all_gather_ms"] = (time.perf_counter() - t0) * 1e3
         res["all_gather_hyps"] = len(allres)
+    return res
+
+
+def bench_beams(budget_s=6.0):
+    """Beam decoders through the reference-facing API (host StepModels, GPU
+    fused expansion + top-k per step) beside the reference-equivalent CPU
+    port (oracle restatement of decoding.py's pure-Python beams), per utterance.
+    CTC and transducer beams: 5K-phrase tree, V=1024, T=50 frames, beam 4
+    (config 3 shape); AED beam: 20K-phrase tree, V=4096, max_len 20, beam 4
+    (config 4 shape, prefix-keyed rows from a seeded bank).  RTFx uses
+    0.04 s frames; AED reports hypotheses/s."""
+    import gen_inputs as gi
+    import paper_2508_07014_b200 as pb
+    from oracle import oracle as orc
+
+    def table(name):
+        phrases, V = gi.corpus(name)
+        ctx = pb.ContextList([pb.Phrase(" ".join(map(str, p)), p) for p in phrases], min_chars=0)
+        return pb.compile_arc_table(pb.compute_fail_links(pb.build_prefix_tree(ctx, pb.TreeParams(), V))), V
+
+    def timed(fn, budget):
+        fn()
+        n, t0 = 0, time.perf_counter()
+        while True:
+            out = fn()
+            n += 1
+            el = time.perf_counter() - t0
+            if el > budget or n >= 20:
+                return el / n, out
+
+    res = {}
+    rng = np.random.default_rng(77)
+    tab5, V = table("p5k_v1024")
+    T, beam = 50, 4
+    lp = gi.random_emissions(rng, T, V)
+    em = pb.EmissionMatrix(lp, blank_id=0)
+    cfg = pb.DecodeConfig(lam=1.0, beam_size=beam)
+    g_s, g_out = timed(lambda: pb.ctc_beam_boosted(em, tab5, cfg)[0].tokens, budget_s / 6)
+    c_s, c_out = timed(lambda: orc.ctc_beam(lp, 0, tab5, 1.0, beam)[0]["tokens"], budget_s / 6)
+    res["ctc_beam"] = {"gpu_ms_per_utt": g_s * 1e3, "cpu_port_ms_per_utt": c_s * 1e3, "rtfx_gpu": T * FRAME_SEC / g_s,
+                       "rtfx_cpu": T * FRAME_SEC / c_s, "same_best": g_out == c_out}
+    rows, default = gi.random_transducer_rows(rng, V)
+    model = pb.TableStepModel(flavor="transducer", default_row=default, rows=rows)
+    step = lambda last, t: rows.get("" if last is None else str(int(last)), default)  # noqa: E731
+    tcfg = pb.DecodeConfig(lam=1.0, beam_size=beam, max_symbols_per_frame=5)
+    g_s, g_out = timed(lambda: pb.transducer_beam_boosted(model, T, 0, tab5, tcfg)[0].tokens, budget_s / 6)
+    c_s, c_out = timed(lambda: orc.transducer_beam(step, T, 0, tab5, 1.0, beam, 5, V)[0]["tokens"], budget_s / 6)
+    res["transducer_beam"] = {"gpu_ms_per_utt": g_s * 1e3, "cpu_port_ms_per_utt": c_s * 1e3,
+                              "rtfx_gpu": T * FRAME_SEC / g_s, "rtfx_cpu": T * FRAME_SEC / c_s, "same_best": g_out == c_out}
+    tab20, V4 = table("p20k_v4096")
+    bank = gi.log_softmax(rng.normal(0, 1.5, size=(64, V4))).astype(np.float32)
+    eos = V4 - 1
+
+    class BankAED(pb.StepModel):
+        flavor, vocab_size, eos_id = "aed", V4, eos
+
+        def logprobs(self, prefix, n):
+            return bank[hash(tuple(prefix)) % 64]
+
+    astep = lambda p, n: bank[hash(tuple(p)) % 64]  # noqa: E731
+    acfg = pb.DecodeConfig(lam=1.0, beam_size=beam)
+    g_s, g_out = timed(lambda: pb.aed_beam_boosted(BankAED(), tab20, acfg, max_len=20)[0].tokens, budget_s / 6)
+    c_s, c_out = timed(lambda: orc.aed_beam(astep, tab20, 1.0, beam, 20, eos, V4)[0]["tokens"], budget_s / 6)
+    res["aed_beam"] = {"gpu_ms_per_utt": g_s * 1e3, "cpu_port_ms_per_utt": c_s * 1e3, "hyps_per_s_gpu": 1 / g_s,
+                       "hyps_per_s_cpu": 1 / c_s, "same_best": g_out == c_out}
+    res["note"] = ("per-utterance calls of the reference-facing API (host StepModel rows, one fused "
+                   "pgpb_beam_topk launch per step/wave); CPU = oracle port of the reference's Python beams, 1 thread")
     return res
 
 
