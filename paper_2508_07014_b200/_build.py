@@ -1,6 +1,6 @@
 """In-tree build of the native library (libpgpb.so) for sm_100a.
 
-`python -m paper_2508_07014_b200._build` (or `__graft_entry__.build()`)
+`python paper_2508_07014_b200/_build.py` (or `__graft_entry__.build()`)
 compiles every translation unit under csrc/ with nvcc
 (-gencode arch=compute_100a,code=sm_100a -lineinfo) and links them into
 paper_2508_07014_b200/libpgpb.so, next to this file, so the library

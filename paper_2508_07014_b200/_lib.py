@@ -84,7 +84,7 @@ def _load() -> ctypes.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
             f"{LIB_PATH} is missing: build the CUDA extension first "
-            "(python -m paper_2508_07014_b200._build); there is no CPU fallback"
+            "(python __graft_entry__.py or python paper_2508_07014_b200/_build.py); there is no CPU fallback"
         )
     lib = ctypes.CDLL(str(LIB_PATH))
     for name, args in _SIGS.items():
