@@ -243,6 +243,95 @@ int pgpb_beam_topk(const pgpb_table *table, const float *d_logprobs, int64_t ld,
                    int32_t *d_out_token, double *d_out_am, double *d_out_boost,
                    int32_t *d_out_next, float *d_out_delta, void *stream);
 
+/* ------------------------------------------------------------------------
+ * Device-resident batched beam search.  The hypothesis bookkeeping the
+ * reference does in Python dicts (decoding.py:428-495 transducer beam,
+ * :502-587 AED beam) runs inside the fused expansion + top-k kernels: one
+ * CTA per utterance scores every (hypothesis, token) candidate, merges and
+ * prunes, and writes the new beam in place.  Token sequences live in an
+ * append-only per-utterance trie of trace nodes; hypotheses carry the node
+ * of their last token plus (length, 64-bit hash) so sequence equality
+ * (_keep_better's dict keys) is a hash filter followed by an exact walk.
+ * Ranking is the reference's R11 (key = am + lam*boost in fp64, then am);
+ * exact (key, am) ties between different hypotheses fall back to the slot
+ * order instead of comparing token tuples.
+ * ---------------------------------------------------------------------- */
+
+/* K hypotheses per utterance, struct of arrays, each [B, K] row-major.   */
+typedef struct pgpb_beam_hyps {
+  double *am;
+  double *boost;
+  int32_t *tree;     /* GPU-PB tree state                                  */
+  int32_t *last;     /* last token (-1: none yet, the start symbol)        */
+  int32_t *node;     /* trace node of the last step (-1: empty sequence)   */
+  int32_t *len;      /* number of tokens                                   */
+  uint64_t *hash;    /* hash of the token sequence (0 for the empty one)   */
+  uint8_t *flags;    /* bit 0 valid, bit 1 ended (AED eos)                 */
+  int32_t *parent;   /* AED: slot of the previous beam this one came from  */
+} pgpb_beam_hyps;
+
+/* Append-only trie of trace steps; utterance b's node i at b*nmax + i.
+ * TraceStep(token, delta, state) of decoding.py:63-69.                    */
+typedef struct pgpb_beam_trace {
+  int32_t *parent;
+  int32_t *token;
+  int32_t *state;
+  double *delta;
+  int32_t *count;    /* [B] nodes in use                                   */
+  int32_t *overflow; /* set to 1 when an utterance runs out of nodes       */
+  int64_t nmax;
+} pgpb_beam_trace;
+
+/* Transducer beam (R9, decoding.py:454-495): every frame runs exactly
+ * cap + 1 waves.  Wave k: each valid hypothesis' blank extension is merged
+ * into the frame's finished pool by token sequence (_keep_better, strict
+ * improvement); for k < cap the top `beam` non-blank expansions become the
+ * next wave's hypotheses; at k == cap the pool's top `beam` become the next
+ * frame's beam and t[b] advances.  Rows: d_logprobs[(b*beam + r)*ld + v] is
+ * step(last[b,r], t[b]).  rollback != 0 (opt-in, no reference counterpart):
+ * at an utterance's last frame every finished hypothesis gets the backoff
+ * total of its state added to its boost (unfinished phrase credit removed)
+ * before the final top-k.  Utterances with t[b] >= lengths[b] are idle.   */
+typedef struct pgpb_tbeam_state {
+  pgpb_beam_hyps hyps;      /* [B, beam]                                   */
+  pgpb_beam_hyps pool;      /* [B, pool_cap] finished (blank-extended)     */
+  int32_t *pool_count;      /* [B]                                         */
+  pgpb_beam_trace trace;
+  int32_t *t;               /* [B] current frame                           */
+  const int32_t *lengths;   /* [B]                                         */
+  int32_t beam;
+  int32_t cap;              /* max_symbols_per_frame                       */
+  int32_t pool_cap;         /* >= beam * (cap + 1)                         */
+  int32_t rollback;
+} pgpb_tbeam_state;
+
+int pgpb_tbeam_wave(const pgpb_table *table, const float *d_logprobs, int64_t ld, int64_t batch,
+                    int32_t vocab_size, int32_t blank, double lam, int32_t use_boost, int32_t wave,
+                    const pgpb_tbeam_state *state, void *stream);
+
+/* AED beam step (R10, decoding.py:532-584): candidates are the beam's
+ * ended / length-capped hypotheses (carried unchanged) plus every token
+ * expansion of the others; eos ends a hypothesis with
+ *   bump = max(0, row_max[state]) + (final_score[state] if is_final)
+ * added to its boost when use_boost && eos_bump.  The top `beam` replace
+ * the beam in place; hyps.parent[b, r] receives the source slot (for the
+ * decoder's KV-cache reorder).  *any_active is OR-ed with 1 when some new
+ * hypothesis can still expand.  Rows: step(prefix of slot r, len).        */
+typedef struct pgpb_aed_state {
+  pgpb_beam_hyps hyps;      /* [B, beam]                                   */
+  pgpb_beam_trace trace;
+  const float *row_max;     /* [S] from pgpb_row_max                       */
+  int32_t *any_active;
+  int32_t beam;
+  int32_t max_len;
+  int32_t eos;
+  int32_t eos_bump;
+} pgpb_aed_state;
+
+int pgpb_aed_step(const pgpb_table *table, const float *d_logprobs, int64_t ld, int64_t batch,
+                  int32_t vocab_size, double lam, int32_t use_boost, const pgpb_aed_state *state,
+                  void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -396,8 +396,22 @@ def _out(beam, lam, k):
             for h in sorted(beam, key=_rank(lam))[:k]]
 
 
-def transducer_beam(step, T, blank, table, lam, beam_size, max_symbols, V, enabled=True):
-    """decoding.py:428-495 (R9)."""
+def backoff_total(table, s: int) -> float:
+    """fp32 sum of backoff weights along s's chain, in chain order (_kernels.pyx:59-66)."""
+    acc = np.float32(0.0)
+    while s != 0:
+        acc = np.float32(acc + np.float32(table.backoff_weight[s]))
+        s = int(table.backoff_to[s])
+    return float(acc)
+
+
+def transducer_beam(step, T, blank, table, lam, beam_size, max_symbols, V, enabled=True, rollback=False):
+    """decoding.py:428-495 (R9).
+
+    rollback=True is an extension with NO reference counterpart (parity
+    unpinned): at the last frame every finished hypothesis gets
+    backoff_total(state) added to its boost before the final pruning.
+    """
     use = _active(table, lam, enabled)
     rank = _rank(lam)
     beam = [_Hyp((), 0.0, 0.0, 0)]
@@ -425,6 +439,9 @@ def transducer_beam(step, T, blank, table, lam, beam_size, max_symbols, V, enabl
                              trace=h.trace + ((v, d, ns),))
                     _keep_better(nxt, (c.tokens, k + 1), c, lam)
             active = dict(sorted(nxt.items(), key=lambda kv: rank(kv[1]))[:beam_size])
+        if rollback and use and t == T - 1:
+            finished = {k: _Hyp(h.tokens, h.am, h.boost + backoff_total(table, h.state), h.state, h.last, h.ended,
+                                h.trace) for k, h in finished.items()}
         beam = sorted(finished.values(), key=rank)[:beam_size]
     return _out(beam, lam, beam_size)
 

@@ -49,6 +49,34 @@ class LabelLoopState(ctypes.Structure):
                                          "deltas", "states")] + [("lmax", c_int64), ("cap", c_int32)]
 
 
+class BeamHyps(ctypes.Structure):
+    """pgpb_beam_hyps (include/pgpb.h): [B, K] struct of arrays."""
+
+    _fields_ = [(n, c_void_p) for n in ("am", "boost", "tree", "last", "node", "len", "hash", "flags", "parent")]
+
+
+class BeamTrace(ctypes.Structure):
+    """pgpb_beam_trace: append-only per-utterance trie of trace steps."""
+
+    _fields_ = [(n, c_void_p) for n in ("parent", "token", "state", "delta", "count", "overflow")] + \
+        [("nmax", c_int64)]
+
+
+class TBeamState(ctypes.Structure):
+    """pgpb_tbeam_state."""
+
+    _fields_ = [("hyps", BeamHyps), ("pool", BeamHyps), ("pool_count", c_void_p), ("trace", BeamTrace),
+                ("t", c_void_p), ("lengths", c_void_p), ("beam", c_int32), ("cap", c_int32), ("pool_cap", c_int32),
+                ("rollback", c_int32)]
+
+
+class AedState(ctypes.Structure):
+    """pgpb_aed_state."""
+
+    _fields_ = [("hyps", BeamHyps), ("trace", BeamTrace), ("row_max", c_void_p), ("any_active", c_void_p),
+                ("beam", c_int32), ("max_len", c_int32), ("eos", c_int32), ("eos_bump", c_int32)]
+
+
 # name -> argtypes (all return int unless listed in _VOID / _OTHER)
 _P = c_void_p
 _SIGS = {
@@ -74,6 +102,9 @@ _SIGS = {
                              POINTER(LabelLoopState), _P, _P, _P, c_void_p],
     "pgpb_beam_topk": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_int32, _P, _P, _P, _P,
                        _P, _P, _P, c_double, c_int32, c_int32, _P, _P, _P, _P, _P, _P, c_void_p],
+    "pgpb_tbeam_wave": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32, c_int32,
+                        POINTER(TBeamState), c_void_p],
+    "pgpb_aed_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_double, c_int32, POINTER(AedState), c_void_p],
 }
 
 # Every symbol include/pgpb.h declares (checked by tests/test_abi.py).

@@ -1,0 +1,619 @@
+// Device-resident batched beam search: transducer waves (pgpb_tbeam_wave)
+// and AED label-synchronous steps (pgpb_aed_step).
+//
+// Reference: transducer_beam_boosted (decoding.py:428-495, R9),
+// aed_beam_boosted (decoding.py:502-587, R10), _keep_better / _rank_key
+// (decoding.py:396-411, R11).  The reference keeps hypotheses in Python
+// dicts keyed by token tuples and loops over V per hypothesis; here one CTA
+// per utterance does, per wave / step:
+//   1. stage the beam (K slots) in shared memory;
+//   2. (transducer) merge every slot's blank extension into the frame's
+//      finished pool: a warp compares (length, hash) of the pool entries in
+//      parallel and confirms a hash hit by walking both trace chains;
+//   3. score every (slot, token) expansion — closure tokens exactly from the
+//      flattened closure, all other tokens from the dense root row shifted by
+//      the state's backoff total — with fp64 keys in the reference's order,
+//      keeping a sorted per-thread top-K list, then K block-wide argmax
+//      rounds;
+//   4. resolve each winner's (score, next state), append its trace node and
+//      write the new beam in place.
+// Nothing of the [K, V] score matrix is materialised.
+
+#include <string>
+
+#include "pgpb_beam.cuh"
+
+namespace pgpb {
+
+constexpr uint8_t kValid = 1, kEnded = 2;
+
+__device__ __forceinline__ uint64_t hash_push(uint64_t h, int v) {
+  uint64_t x = h * 0x100000001B3ull + (uint64_t(uint32_t(v)) + 0x9E3779B97F4A7C15ull);
+  x ^= x >> 31;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+
+__device__ __forceinline__ double rank_key(double am, double boost, double lam) {
+  return __dadd_rn(am, __dmul_rn(lam, boost));
+}
+
+// Token sequences ending at trace nodes a and b (same utterance, same
+// length) are equal?  Shared prefixes end the walk early (a == b).
+__device__ bool same_tokens(const int32_t *parent, const int32_t *token, int a, int b) {
+  while (a != b) {
+    if (a < 0 || b < 0) return false;
+    if (__ldcg(token + a) != __ldcg(token + b)) return false;
+    a = __ldcg(parent + a);
+    b = __ldcg(parent + b);
+  }
+  return true;
+}
+
+// Beam staged in shared memory.
+struct SBeam {
+  double am[kMaxTopK], boost[kMaxTopK], extra[kMaxTopK];
+  uint64_t hash[kMaxTopK];
+  int tree[kMaxTopK], last[kMaxTopK], node[kMaxTopK], len[kMaxTopK], flags[kMaxTopK];
+};
+
+__device__ __forceinline__ void stage_beam(const pgpb_beam_hyps &H, int64_t base, int beam, SBeam &s) {
+  for (int h = threadIdx.x; h < beam; h += blockDim.x) {
+    s.am[h] = H.am[base + h];
+    s.boost[h] = H.boost[base + h];
+    s.tree[h] = H.tree[base + h];
+    s.last[h] = H.last[base + h];
+    s.node[h] = H.node[base + h];
+    s.len[h] = H.len[base + h];
+    s.hash[h] = H.hash[base + h];
+    s.flags[h] = H.flags[base + h];
+    s.extra[h] = 0.0;
+  }
+}
+
+// Per-thread candidate scan over the expandable slots: dense tokens from the
+// root row shifted by the backoff total, closure tokens exactly.  `skip` is
+// the token that is not an expansion (transducer blank), `special` a token
+// scored with boost `extra[h]` instead of the tree (AED eos), -1 for none.
+template <int K, bool kVec>
+__device__ __forceinline__ void scan_candidates(const TableView &t, const float *root, const unsigned *bm,
+                                                int bm_words, const float *lp, int64_t ld, int64_t row0, int V,
+                                                const SBeam &s, const bool *expand, int beam, int skip, int special,
+                                                double lam, bool use_boost, Cand (&list)[K]) {
+  for (int h = 0; h < beam; ++h) {
+    if (!expand[h]) continue;
+    const float *row = lp + (row0 + h) * ld;
+    const double am_h = s.am[h], boost_h = s.boost[h];
+    float acc = 0.0f;
+    int4 rec = make_int4(0, 0, 0, 0);
+    if (use_boost) {
+      rec = __ldg(t.clo_rec + s.tree[h]);
+      acc = __int_as_float(rec.z);
+    }
+    const unsigned *hbm = bm + h * bm_words;
+    auto consider = [&](int v, float x, double bv) {
+      const double amv = __dadd_rn(am_h, static_cast<double>(x));
+      list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + v});
+    };
+    auto dense = [&](int v, float x) {
+      if (v == skip) return;
+      if (v == special) {
+        consider(v, x, __dadd_rn(boost_h, s.extra[h]));
+        return;
+      }
+      if (use_boost) {
+        if ((hbm[v >> 5] >> (v & 31)) & 1u) return;
+        consider(v, x, __dadd_rn(boost_h, static_cast<double>(acc + root[v])));
+      } else {
+        consider(v, x, boost_h);
+      }
+    };
+    if (kVec) {
+      const float4 *row4 = reinterpret_cast<const float4 *>(row);
+      for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) {
+        const float4 x4 = __ldg(row4 + i);
+        dense(4 * i, x4.x);
+        dense(4 * i + 1, x4.y);
+        dense(4 * i + 2, x4.z);
+        dense(4 * i + 3, x4.w);
+      }
+    } else {
+      for (int v = threadIdx.x; v < V; v += blockDim.x) dense(v, __ldg(row + v));
+    }
+    if (use_boost) {
+      for (int i = threadIdx.x; i < rec.y; i += blockDim.x) {
+        const int4 e = __ldg(t.clo + rec.x + i);
+        if (e.x == skip || e.x == special) continue;
+        consider(e.x, __ldg(row + e.x), __dadd_rn(boost_h, static_cast<double>(__int_as_float(e.z))));
+      }
+    }
+  }
+}
+
+// k rounds of block-wide argmax over the per-thread list heads.
+template <int K>
+__device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp, int *s_win, double *s_key,
+                                           double *s_am) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = 0; r < k; ++r) {
+    Cand best = list[0];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const Cand oc = shfl_cand(best, o);
+      if (cand_better(oc, best)) best = oc;
+    }
+    if (lane == 0) s_warp[wid] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Cand b = s_warp[0];
+      for (int w = 1; w < nw; ++w)
+        if (cand_better(s_warp[w], b)) b = s_warp[w];
+      s_win[r] = b.cid;
+      s_key[r] = b.key;
+      s_am[r] = b.am;
+    }
+    __syncthreads();
+    if (s_win[r] != INT_MAX && list[0].cid == s_win[r]) list_pop<K>(list);
+  }
+  __syncthreads();
+}
+
+// Mark each expandable slot's closure tokens in its bitmap.
+__device__ __forceinline__ void mark_closures(const TableView &t, unsigned *bm, int bm_words, const SBeam &s,
+                                              const bool *expand, int beam) {
+  for (int i = threadIdx.x; i < beam * bm_words; i += blockDim.x) bm[i] = 0u;
+  __syncthreads();
+  for (int h = 0; h < beam; ++h) {
+    if (!expand[h]) continue;
+    const int4 rec = __ldg(t.clo_rec + s.tree[h]);
+    for (int i = threadIdx.x; i < rec.y; i += blockDim.x) {
+      const int tok = __ldg(&t.clo[rec.x + i].x);
+      atomicOr(bm + h * bm_words + (tok >> 5), 1u << (tok & 31));
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void setup_root(const TableView &t, bool use_boost, int smem_root, unsigned char *smem,
+                                           const float *&root, unsigned *&bm) {
+  root = t.root_scores;
+  size_t off = 0;
+  if (use_boost && smem_root) {
+    float *s_root = reinterpret_cast<float *>(smem);
+    const int n4 = t.vocab_padded >> 2;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x)
+      reinterpret_cast<float4 *>(s_root)[i] = __ldg(reinterpret_cast<const float4 *>(t.root_scores) + i);
+    root = s_root;
+    off = size_t(t.vocab_padded) * 4;
+  }
+  bm = reinterpret_cast<unsigned *>(smem + off);
+}
+
+// ---------------------------------------------------------------------------
+// Transducer wave
+
+struct TBeamArgs {
+  TableView t;
+  const float *lp;
+  int64_t ld;
+  int V;
+  int blank;
+  double lam;
+  int use_boost;
+  int wave;
+  int smem_root;
+  pgpb_tbeam_state s;
+};
+
+__device__ __forceinline__ void write_hyp(const pgpb_beam_hyps &H, int64_t i, double am, double boost, int tree,
+                                          int last, int node, int len, uint64_t hash, uint8_t flags) {
+  H.am[i] = am;
+  H.boost[i] = boost;
+  H.tree[i] = tree;
+  H.last[i] = last;
+  H.node[i] = node;
+  H.len[i] = len;
+  H.hash[i] = hash;
+  H.flags[i] = flags;
+}
+
+template <int K, bool kVec>
+__global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ SBeam s;
+  __shared__ bool s_expand[kMaxTopK];
+  __shared__ Cand s_warp[kBeamThreads / 32];
+  __shared__ int s_win[kMaxTopK];
+  __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
+  __shared__ int s_node_base;
+  const pgpb_tbeam_state &S = a.s;
+  const int b = blockIdx.x;
+  const int t = S.t[b];
+  if (t >= S.lengths[b]) return;
+  const TableView &tv = a.t;
+  const int V = a.V, beam = S.beam;
+  const bool use_boost = a.use_boost != 0;
+  const int64_t hb = int64_t(b) * beam;
+  const int64_t nb = int64_t(b) * S.trace.nmax;
+  const int32_t *np = S.trace.parent + nb, *nt = S.trace.token + nb;
+  const float *root;
+  unsigned *bm;
+  setup_root(tv, use_boost, a.smem_root, smem, root, bm);
+  stage_beam(S.hyps, hb, beam, s);
+  const bool expand_wave = a.wave < S.cap;
+  for (int h = threadIdx.x; h < beam; h += blockDim.x) s_expand[h] = expand_wave && (s.flags[h] & kValid);
+  if (threadIdx.x == 0) s_node_base = S.trace.count[b];
+  __syncthreads();
+
+  // 1. blank extensions -> finished pool, in rank (slot) order (warp 0)
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int64_t pb = int64_t(b) * S.pool_cap;
+    int cnt = S.pool_count[b];
+    for (int h = 0; h < beam; ++h) {
+      if (!(s.flags[h] & kValid)) continue;
+      const double am_e = __dadd_rn(s.am[h], static_cast<double>(__ldg(a.lp + (hb + h) * a.ld + a.blank)));
+      const double bo_e = s.boost[h];
+      int match = -1;
+      for (int j0 = 0; j0 < cnt && match < 0; j0 += 32) {
+        const int j = j0 + lane;
+        bool eq = false;
+        if (j < cnt && S.pool.len[pb + j] == s.len[h] && S.pool.hash[pb + j] == s.hash[h])
+          eq = same_tokens(np, nt, S.pool.node[pb + j], s.node[h]);
+        const unsigned m = __ballot_sync(kFull, eq);
+        if (m) match = j0 + __ffs(m) - 1;
+      }
+      if (lane == 0) {
+        int dst = -1;
+        if (match >= 0) {
+          const double oa = S.pool.am[pb + match];
+          const double ok = rank_key(oa, S.pool.boost[pb + match], a.lam);
+          const double ck = rank_key(am_e, bo_e, a.lam);
+          if (ck > ok || (ck == ok && am_e > oa)) dst = match;  // decoding.py:396-404
+        } else if (cnt < S.pool_cap) {
+          dst = cnt;
+        }
+        if (dst >= 0)
+          write_hyp(S.pool, pb + dst, am_e, bo_e, s.tree[h], s.last[h], s.node[h], s.len[h], s.hash[h], kValid);
+      }
+      if (match < 0 && cnt < S.pool_cap) ++cnt;
+      __syncwarp();
+    }
+    if (lane == 0) S.pool_count[b] = cnt;
+  }
+
+  if (expand_wave) {
+    // 2. top-beam non-blank expansions -> next wave
+    const int bm_words = (V + 31) >> 5;
+    if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam);
+    Cand list[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+    scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, a.blank, -1, a.lam,
+                             use_boost, list);
+    block_topk<K>(list, beam, s_warp, s_win, s_key, s_am);
+    for (int r = threadIdx.x; r < beam; r += blockDim.x) {
+      const int cid = s_win[r];
+      const int64_t o = hb + r;
+      if (cid == INT_MAX) {
+        S.hyps.flags[o] = 0;
+        continue;
+      }
+      const int h = cid / V, v = cid % V;
+      float sc = 0.0f;
+      int nx = 0;
+      if (use_boost) resolve_cell(tv, tv.root_scores, tv.root_next, s.tree[h], v, sc, nx);
+      const int node = s_node_base + r;  // winners fill slots 0.. contiguously
+      if (node >= S.trace.nmax) {
+        *S.trace.overflow = 1;
+        S.hyps.flags[o] = 0;
+        continue;
+      }
+      S.trace.parent[nb + node] = s.node[h];
+      S.trace.token[nb + node] = v;
+      S.trace.state[nb + node] = nx;
+      S.trace.delta[nb + node] = static_cast<double>(sc);
+      write_hyp(S.hyps, o, s_am[r], __dadd_rn(s.boost[h], static_cast<double>(sc)), nx, v, node, s.len[h] + 1,
+                hash_push(s.hash[h], v), kValid);
+    }
+    if (threadIdx.x == 0) {
+      int n = 0;
+      while (n < beam && s_win[n] != INT_MAX) ++n;
+      const int64_t lim = S.trace.nmax;
+      S.trace.count[b] = int(s_node_base + n < lim ? s_node_base + n : lim);
+    }
+    return;
+  }
+
+  // 3. last wave: the pool's top-beam becomes the next frame's beam
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int64_t pb = int64_t(b) * S.pool_cap;
+    const int cnt = S.pool_count[b];
+    const bool final_frame = (t + 1 == S.lengths[b]);
+    if (final_frame && S.rollback && use_boost) {
+      for (int j = lane; j < cnt; j += 32) {
+        const float accv = __int_as_float(__ldg(&tv.clo_rec[S.pool.tree[pb + j]].z));
+        S.pool.boost[pb + j] = __dadd_rn(S.pool.boost[pb + j], static_cast<double>(accv));
+      }
+      __syncwarp();
+    }
+    unsigned long long taken = 0ull;  // entries lane + 32*i already selected
+    for (int r = 0; r < beam; ++r) {
+      double bk = -INFINITY, ba = -INFINITY;
+      int bj = INT_MAX;
+      for (int i = 0, j = lane; j < cnt; ++i, j += 32) {
+        if ((taken >> i) & 1ull) continue;
+        const double am = S.pool.am[pb + j];
+        const double k = rank_key(am, S.pool.boost[pb + j], a.lam);
+        if (k > bk || (k == bk && (am > ba || (am == ba && j < bj)))) {
+          bk = k;
+          ba = am;
+          bj = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ok = __shfl_xor_sync(kFull, bk, o), oa = __shfl_xor_sync(kFull, ba, o);
+        const int oj = __shfl_xor_sync(kFull, bj, o);
+        if (ok > bk || (ok == bk && (oa > ba || (oa == ba && oj < bj)))) {
+          bk = ok;
+          ba = oa;
+          bj = oj;
+        }
+      }
+      if (bj != INT_MAX && (bj & 31) == lane) taken |= 1ull << (bj >> 5);
+      if (lane == 0) {
+        const int64_t o = hb + r;
+        if (bj == INT_MAX) {
+          S.hyps.flags[o] = 0;
+        } else {
+          const int64_t q = pb + bj;
+          write_hyp(S.hyps, o, S.pool.am[q], S.pool.boost[q], S.pool.tree[q], S.pool.last[q], S.pool.node[q],
+                    S.pool.len[q], S.pool.hash[q], kValid);
+        }
+      }
+    }
+    if (lane == 0) {
+      S.pool_count[b] = 0;
+      S.t[b] = t + 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// AED step
+
+struct AedArgs {
+  TableView t;
+  const float *lp;
+  int64_t ld;
+  int V;
+  double lam;
+  int use_boost;
+  int smem_root;
+  pgpb_aed_state s;
+};
+
+template <int K, bool kVec>
+__global__ void __launch_bounds__(kBeamThreads) aed_step_kernel(AedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ SBeam s;
+  __shared__ bool s_expand[kMaxTopK];
+  __shared__ Cand s_warp[kBeamThreads / 32];
+  __shared__ int s_win[kMaxTopK];
+  __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
+  __shared__ int s_node_base, s_any;
+  const pgpb_aed_state &S = a.s;
+  const int b = blockIdx.x;
+  const TableView &tv = a.t;
+  const int V = a.V, beam = S.beam, eos = S.eos;
+  const bool use_boost = a.use_boost != 0;
+  const int64_t hb = int64_t(b) * beam;
+  const int64_t nb = int64_t(b) * S.trace.nmax;
+  const float *root;
+  unsigned *bm;
+  setup_root(tv, use_boost, a.smem_root, smem, root, bm);
+  stage_beam(S.hyps, hb, beam, s);
+  if (threadIdx.x == 0) {
+    s_node_base = S.trace.count[b];
+    s_any = 0;
+  }
+  __syncthreads();
+  for (int h = threadIdx.x; h < beam; h += blockDim.x) {
+    const bool ex = (s.flags[h] & kValid) && !(s.flags[h] & kEnded) && s.len[h] < S.max_len;
+    s_expand[h] = ex;
+    if (ex) atomicOr(&s_any, 1);
+    // eos bump (decoding.py:546-552): max(0, max_v srow) + final score
+    double bump = 0.0;
+    if (ex && use_boost && S.eos_bump) {
+      const float best = __ldg(S.row_max + s.tree[h]);
+      bump = best > 0.0f ? static_cast<double>(best) : 0.0;
+      const int4 rec = __ldg(tv.clo_rec + s.tree[h]);
+      if (rec.w) bump = __dadd_rn(bump, static_cast<double>(__ldg(tv.final_score + s.tree[h])));
+    }
+    s.extra[h] = bump;
+  }
+  __syncthreads();
+  if (!s_any) {  // nothing left to expand: the beam stays as it is
+    for (int r = threadIdx.x; r < beam; r += blockDim.x) S.hyps.parent[hb + r] = r;
+    return;
+  }
+  const int bm_words = (V + 31) >> 5;
+  if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam);
+  Cand list[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+  scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, -1, eos, a.lam, use_boost,
+                           list);
+  // carried hypotheses (ended or at max_len), ranked unchanged
+  for (int h = threadIdx.x; h < beam; h += blockDim.x)
+    if ((s.flags[h] & kValid) && !s_expand[h])
+      list_insert<K>(list, Cand{rank_key(s.am[h], s.boost[h], a.lam), s.am[h], beam * V + h});
+  block_topk<K>(list, beam, s_warp, s_win, s_key, s_am);
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  // Winners that create a trace node get consecutive node ids in rank order.
+  for (int r = threadIdx.x; r < beam; r += blockDim.x) {
+    const int cid = s_win[r];
+    const int64_t o = hb + r;
+    if (cid == INT_MAX) {
+      S.hyps.flags[o] = 0;
+      S.hyps.parent[o] = r;
+      continue;
+    }
+    if (cid >= beam * V) {  // carried
+      const int h = cid - beam * V;
+      write_hyp(S.hyps, o, s.am[h], s.boost[h], s.tree[h], s.last[h], s.node[h], s.len[h], s.hash[h],
+                static_cast<uint8_t>(s.flags[h]));
+      S.hyps.parent[o] = h;
+      continue;
+    }
+    int node = s_node_base;
+    for (int q = 0; q < r; ++q) node += (s_win[q] != INT_MAX && s_win[q] < beam * V);
+    const int h = cid / V, v = cid % V;
+    S.hyps.parent[o] = h;
+    if (node >= S.trace.nmax) {
+      *S.trace.overflow = 1;
+      S.hyps.flags[o] = 0;
+      continue;
+    }
+    S.trace.parent[nb + node] = s.node[h];
+    S.trace.token[nb + node] = v;
+    if (v == eos) {  // ended, tokens / state / last unchanged; trace gets (eos, bump, state)
+      S.trace.state[nb + node] = s.tree[h];
+      S.trace.delta[nb + node] = s.extra[h];
+      write_hyp(S.hyps, o, s_am[r], __dadd_rn(s.boost[h], s.extra[h]), s.tree[h], s.last[h], node, s.len[h],
+                s.hash[h], kValid | kEnded);
+    } else {
+      float sc = 0.0f;
+      int nx = 0;
+      if (use_boost) resolve_cell(tv, tv.root_scores, tv.root_next, s.tree[h], v, sc, nx);
+      S.trace.state[nb + node] = nx;
+      S.trace.delta[nb + node] = static_cast<double>(sc);
+      write_hyp(S.hyps, o, s_am[r], __dadd_rn(s.boost[h], static_cast<double>(sc)), nx, v, node, s.len[h] + 1,
+                hash_push(s.hash[h], v), kValid);
+      if (s.len[h] + 1 < S.max_len) atomicOr(&s_any, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int q = 0; q < beam; ++q) n += (s_win[q] != INT_MAX && s_win[q] < beam * V);
+    const int64_t lim = S.trace.nmax;
+    S.trace.count[b] = int(s_node_base + n < lim ? s_node_base + n : lim);
+    if (s_any) atomicOr(S.any_active, 1);
+  }
+}
+
+static size_t beam_smem(const TableView &t, bool use_boost, int beam, int &smem_root) {
+  const size_t bm = use_boost ? size_t(beam) * size_t((t.vocab_size + 31) >> 5) * 4 : 0;
+  const size_t root = size_t(t.vocab_padded) * 4;
+  smem_root = (use_boost && root + bm <= size_t(kMaxSmemRootBytes)) ? 1 : 0;
+  return bm + (smem_root ? root : 0);
+}
+
+template <typename Fn, typename Args>
+static int launch_beam(Fn fn, const Args &args, size_t smem, int64_t grid, cudaStream_t st) {
+  if (smem > 48 * 1024)
+    PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  fn<<<static_cast<unsigned>(grid), kBeamThreads, smem, st>>>(args);
+  PGPB_CUDA_TRY(cudaGetLastError());
+  return PGPB_OK;
+}
+
+static int check_common(const pgpb_table *table, int64_t ld, int64_t batch, int V, int beam, int use_boost) {
+  if (batch < 0 || V < 2 || ld < V) return fail(PGPB_EINVAL, "bad shape");
+  if (beam < 1 || beam > kMaxTopK) return fail(PGPB_EINVAL, "beam must be in [1, 32]");
+  if (int64_t(beam) * V + beam >= INT_MAX) return fail(PGPB_EINVAL, "beam * V too large");
+  if (use_boost && !table) return fail(PGPB_EINVAL, "use_boost requires a table");
+  if (table && table->view.vocab_size != V)
+    return fail(PGPB_EINVAL, "vocab size " + std::to_string(V) + " != table vocab size " +
+                                 std::to_string(table->view.vocab_size));
+  return PGPB_OK;
+}
+
+static TableView view_or_empty(const pgpb_table *table, int V) {
+  TableView v{};
+  if (table) return table->view;
+  v.vocab_size = V;
+  v.vocab_padded = (V + 3) & ~3;
+  return v;
+}
+
+}  // namespace pgpb
+
+extern "C" {
+
+int pgpb_tbeam_wave(const pgpb_table *table, const float *d_lp, int64_t ld, int64_t batch, int32_t V,
+                    int32_t blank, double lam, int32_t use_boost, int32_t wave, const pgpb_tbeam_state *state,
+                    void *stream) {
+  using namespace pgpb;
+  if (!state) return fail(PGPB_EINVAL, "NULL state");
+  int rc = check_common(table, ld, batch, V, state->beam, use_boost);
+  if (rc) return rc;
+  if (blank < 0 || blank >= V) return fail(PGPB_EINVAL, "blank out of range");
+  if (wave < 0 || wave > state->cap || state->cap < 1) return fail(PGPB_EINVAL, "bad wave index");
+  if (state->pool_cap < state->beam * (state->cap + 1) || state->pool_cap > 64 * 32)
+    return fail(PGPB_EINVAL, "pool_cap must be in [beam*(cap+1), 2048]");
+  if (batch == 0) return PGPB_OK;
+  TBeamArgs a{};
+  a.t = view_or_empty(table, V);
+  a.lp = d_lp;
+  a.ld = ld;
+  a.V = V;
+  a.blank = blank;
+  a.lam = lam;
+  a.use_boost = use_boost ? 1 : 0;
+  a.wave = wave;
+  a.s = *state;
+  const size_t smem = beam_smem(a.t, use_boost, state->beam, a.smem_root);
+  const bool vec = (V % 4) == 0 && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(d_lp) % 16) == 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int k = state->beam;
+#define PGPB_TB(KK) \
+  return vec ? launch_beam(tbeam_wave_kernel<KK, true>, a, smem, batch, st) : launch_beam(tbeam_wave_kernel<KK, false>, a, smem, batch, st)
+  if (k <= 4) PGPB_TB(4);
+  if (k <= 8) PGPB_TB(8);
+  if (k <= 16) PGPB_TB(16);
+  PGPB_TB(32);
+#undef PGPB_TB
+}
+
+int pgpb_aed_step(const pgpb_table *table, const float *d_lp, int64_t ld, int64_t batch, int32_t V, double lam,
+                  int32_t use_boost, const pgpb_aed_state *state, void *stream) {
+  using namespace pgpb;
+  if (!state) return fail(PGPB_EINVAL, "NULL state");
+  int rc = check_common(table, ld, batch, V, state->beam, use_boost);
+  if (rc) return rc;
+  if (state->eos < 0 || state->eos >= V) return fail(PGPB_EINVAL, "eos out of range");
+  if (state->max_len < 1) return fail(PGPB_EINVAL, "max_len must be >= 1");
+  if (use_boost && state->eos_bump && !state->row_max) return fail(PGPB_EINVAL, "row_max required for the eos bump");
+  if (batch == 0) return PGPB_OK;
+  AedArgs a{};
+  a.t = view_or_empty(table, V);
+  a.lp = d_lp;
+  a.ld = ld;
+  a.V = V;
+  a.lam = lam;
+  a.use_boost = use_boost ? 1 : 0;
+  a.s = *state;
+  const size_t smem = beam_smem(a.t, use_boost, state->beam, a.smem_root);
+  const bool vec = (V % 4) == 0 && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(d_lp) % 16) == 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int k = state->beam;
+#define PGPB_AE(KK) \
+  return vec ? launch_beam(aed_step_kernel<KK, true>, a, smem, batch, st) : launch_beam(aed_step_kernel<KK, false>, a, smem, batch, st)
+  if (k <= 4) PGPB_AE(4);
+  if (k <= 8) PGPB_AE(8);
+  if (k <= 16) PGPB_AE(16);
+  PGPB_AE(32);
+#undef PGPB_AE
+}
+
+}  // extern "C"
