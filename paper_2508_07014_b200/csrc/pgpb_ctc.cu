@@ -37,6 +37,12 @@
 
 namespace pgpb {
 
+// Production path (pgpb_ctc_spec.cu).
+int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64_t T, int32_t V,
+                     const int32_t *d_lengths, int32_t blank, double lam, int32_t use_boost, int32_t *d_tokens,
+                     double *d_deltas, int32_t *d_states, int32_t *d_num_out, double *d_am, double *d_boost,
+                     cudaStream_t st);
+
 constexpr int kTopM = 4;
 
 #ifdef PGPB_SEQ_PROFILE
@@ -568,6 +574,12 @@ int pgpb_ctc_greedy(const pgpb_table *table, const float *d_lp, int64_t B, int64
                                  std::to_string(table->view.vocab_size));
   if (B == 0) return PGPB_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // The two-phase kernels below (parallel top-M + one warp per utterance)
+  // stay reachable for A/B measurements: PGPB_CTC_TWOPHASE=1.
+  const bool two_phase = getenv("PGPB_CTC_TWOPHASE") && atoi(getenv("PGPB_CTC_TWOPHASE")) != 0;
+  if (!two_phase)
+    return ctc_spec_launch(table, d_lp, B, T, V, d_lengths, blank, lam, use_boost, d_tokens, d_deltas, d_states,
+                            d_num_out, d_am, d_boost, st);
   retain_pool(current_device());
   const int M = use_boost ? kTopM : 1;
   const int64_t F = B * (T > 0 ? T : 1);

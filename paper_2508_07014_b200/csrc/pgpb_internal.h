@@ -24,6 +24,7 @@ struct TableView {
   int32_t num_arcs;
   float unk_score;
   float max_root_score;
+  float typ_gain;              // max over the root's children of (best closure score - best dense score)
   const float *root_scores;    // [Vp] f32: unk background, root arcs on top (table.py:74-81)
   const int32_t *root_next;    // [Vp]
   const int4 *state_rec;       // [S] {arc_start, arc_end, backoff_to, bits(backoff_weight)}
@@ -39,6 +40,13 @@ struct TableView {
   const int4 *blob;            // [S + C]
   const int32_t *blob_off;     // [S]
   const int32_t *root_next_off;  // [Vp] blob_off[root_next[v]]
+  // Per state: bitmap of its closure tokens (Vw = ceil(V/32) words per
+  // state), so a decoder tests "is v a first-hit arc of s" with one load
+  // instead of a scan; NULL when S * Vw words would exceed the cap.  The
+  // blob header's 4th field holds the state's largest closure-arc score
+  // (bits of an f32, -inf when the closure is empty).
+  const uint32_t *clo_bits;    // [S][Vw]
+  int32_t bits_words;          // Vw
 };
 
 }  // namespace pgpb

@@ -10,6 +10,7 @@
 // (record, entries) load pair then resolves any state.
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -124,12 +125,29 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   for (int32_t s0 = 0; s0 < S; ++s0) {
     const int4 r = clo_rec[s0];
     int4 *b = blob.data() + boff[s0];
-    b[0] = make_int4(r.y, r.z, s0, 0);
+    float smax = -INFINITY;
     for (int32_t i = 0; i < r.y; ++i) {
       const int4 e = clo[static_cast<size_t>(r.x) + i];
       b[1 + i] = make_int4(e.x, e.y, e.z, boff[e.y]);
+      float sc;
+      std::memcpy(&sc, &e.z, 4);
+      smax = std::max(smax, sc);
     }
+    b[0] = make_int4(r.y, r.z, s0, f2i(smax));
   }
+  // Closure-token bitmaps (capped at 512 MiB).
+  const int32_t Vw = (V + 31) / 32;
+  const bool with_bits = int64_t(S) * Vw * 4 <= (int64_t(512) << 20);
+  std::vector<uint32_t> bits(with_bits ? static_cast<size_t>(S) * Vw : 1, 0u);
+  if (with_bits)
+    for (int32_t s0 = 0; s0 < S; ++s0) {
+      const int4 r = clo_rec[s0];
+      uint32_t *w = bits.data() + static_cast<size_t>(s0) * Vw;
+      for (int32_t i = 0; i < r.y; ++i) {
+        const int32_t v = clo[static_cast<size_t>(r.x) + i].x;
+        w[v >> 5] |= 1u << (v & 31);
+      }
+    }
   std::vector<int32_t> rn_off(static_cast<size_t>(Vp), 0);
   for (int32_t v = 0; v < Vp; ++v) rn_off[v] = boff[root_next[v]];
 
@@ -150,6 +168,7 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   const int64_t o_blob = place(int64_t(blob.size()) * 16);
   const int64_t o_boff = place(int64_t(S) * 4);
   const int64_t o_rno = place(int64_t(Vp) * 4);
+  const int64_t o_bits = place(int64_t(bits.size()) * 4);
   const int64_t total = off;
 
   int prev_dev = 0;
@@ -172,6 +191,7 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   std::memcpy(staging.data() + o_blob, blob.data(), blob.size() * 16);
   std::memcpy(staging.data() + o_boff, boff.data(), size_t(S) * 4);
   std::memcpy(staging.data() + o_rno, rn_off.data(), size_t(Vp) * 4);
+  std::memcpy(staging.data() + o_bits, bits.data(), bits.size() * 4);
   e = cudaMemcpy(arena, staging.data(), static_cast<size_t>(total), cudaMemcpyHostToDevice);
   cudaSetDevice(prev_dev);
   if (e != cudaSuccess) {
@@ -193,6 +213,21 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   v.num_arcs = A;
   v.unk_score = unk_score;
   v.max_root_score = max_root;
+  {  // typical advantage of a first-hit arc over the dense row (depth-1 states)
+    float g = 0.0f;
+    for (int32_t j = state_start[0]; j < state_end[0]; ++j) {
+      const int4 r = clo_rec[arc_to[j]];
+      float acc, smax = -INFINITY;
+      std::memcpy(&acc, &r.z, 4);
+      for (int32_t i = 0; i < r.y; ++i) {
+        float sc;
+        std::memcpy(&sc, &clo[static_cast<size_t>(r.x) + i].z, 4);
+        smax = std::max(smax, sc);
+      }
+      if (r.y > 0) g = std::max(g, smax - (acc + max_root));
+    }
+    v.typ_gain = g;
+  }
   v.root_scores = reinterpret_cast<const float *>(arena + o_rs);
   v.root_next = reinterpret_cast<const int32_t *>(arena + o_rn);
   v.state_rec = reinterpret_cast<const int4 *>(arena + o_sr);
@@ -203,6 +238,8 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   v.blob = reinterpret_cast<const int4 *>(arena + o_blob);
   v.blob_off = reinterpret_cast<const int32_t *>(arena + o_boff);
   v.root_next_off = reinterpret_cast<const int32_t *>(arena + o_rno);
+  v.clo_bits = with_bits ? reinterpret_cast<const uint32_t *>(arena + o_bits) : nullptr;
+  v.bits_words = Vw;
   *out = t;
   return PGPB_OK;
 }

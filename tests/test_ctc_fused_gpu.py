@@ -1,0 +1,196 @@
+"""Fused speculative chunk-parallel greedy CTC (pgpb_ctc_fused.cu) vs the oracle.
+
+The fused kernel decides every chunk of frames from a guessed start and
+repairs the guesses in fix-up rounds; these tests drive the regimes that
+stress that: phrase-dense emissions whose tree states stay deep across chunk
+boundaries, heavy boosting that changes many decisions, long utterances that
+run in several segments, every consumer-warp count, ragged lengths, small
+trees whose root row is mostly unk (uncertified dense tokens -> warp rescans),
+and vocabularies that are not a multiple of 4 (scalar row loads).  Results
+must equal the reference restatement (oracle/pgpb_oracle.c, pinned to the
+reference's compiled kernel) bit for bit: tokens, am, boost and the trace.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import gen_inputs as gi
+from conftest import product_table, res_tuple
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _phrase_emissions(rng, phrases, T, V, noise=0.6, hit=4.0, blank_every=2):
+    """Log-probs whose argmax path spells random phrases back to back (with
+    blanks), plus near-miss competitors, so boosted states go deep."""
+    logits = rng.normal(0.0, noise, size=(T, V))
+    t = 0
+    while t < T:
+        ph = phrases[int(rng.integers(len(phrases)))]
+        for tok in ph:
+            if t >= T:
+                break
+            logits[t, tok] += hit
+            logits[t, int(rng.integers(1, V))] += hit + float(rng.normal(0.0, 0.4))
+            t += 1
+            for _ in range(int(rng.integers(0, blank_every + 1))):
+                if t >= T:
+                    break
+                logits[t, 0] += hit
+                t += 1
+    return gi.log_softmax(logits).astype(np.float32)
+
+
+def _run(lps, lens, tab, lam, env=None):
+    from paper_2508_07014_b200 import DecodeConfig, ctc_greedy_boosted_batch
+
+    old = {}
+    for k, v in (env or {}).items():
+        old[k] = os.environ.get(k)
+        os.environ[k] = v
+    try:
+        return ctc_greedy_boosted_batch(lps, lens, tab, DecodeConfig(lam=lam), blank_id=0, want_trace=True)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _check(got, lps, lens, tab, lam):
+    for b in range(lps.shape[0]):
+        n = lps.shape[1] if lens is None else int(lens[b])
+        e = orc.ctc_greedy_decode(lps[b, :n], 0, tab, lam)
+        g = res_tuple(got[b])
+        assert g["tokens"] == e["tokens"], b
+        assert g["am"] == e["am"] and g["boost"] == e["boost"], b
+        assert g["trace"] == [list(x) for x in e["trace"]], b
+
+
+@pytest.fixture(scope="module")
+def t20k():
+    phrases, V = gi.corpus("p20k_v1024")
+    return phrases, V, product_table(phrases, V)
+
+
+@pytest.mark.parametrize("seq", ["0", "1", "2"])
+@pytest.mark.parametrize("lam", [0.0, 1.0, 2.5])
+def test_phrase_dense_deep_states(t20k, lam, seq):
+    """seq: PGPB_CTC_SEQ 0 = automatic mode choice, 1 = sequential walk,
+    2 = speculative rounds only."""
+    phrases, V, tab = t20k
+    rng = np.random.default_rng(31)
+    B, T = 24, 400
+    lps = np.stack([_phrase_emissions(rng, phrases, T, V) for _ in range(B)])
+    _check(_run(lps, None, tab, lam, {"PGPB_CTC_SEQ": seq}), lps, None, tab, lam)
+
+
+@pytest.mark.parametrize("env", [{"PGPB_CTC_CONSUMERS": "1"}, {"PGPB_CTC_CONSUMERS": "2"},
+                                 {"PGPB_CTC_CONSUMERS": "4"}, {"PGPB_CTC_SEGMENT": "97"},
+                                 {"PGPB_CTC_SEGMENT": "300", "PGPB_CTC_CONSUMERS": "3"},
+                                 {"PGPB_CTC_SEGMENT": "200", "PGPB_CTC_SEQ": "1"},
+                                 {"PGPB_CTC_SEGMENT": "111", "PGPB_CTC_SEQ": "2", "PGPB_CTC_CONSUMERS": "1"}])
+def test_segments_and_consumer_counts(t20k, env):
+    phrases, V, tab = t20k
+    rng = np.random.default_rng(32)
+    B, T = 6, 1500
+    lps = np.stack([_phrase_emissions(rng, phrases, T, V, blank_every=1) for _ in range(B)])
+    lens = rng.integers(1, T + 1, size=B).astype(np.int32)
+    lens[0] = T
+    lens[1] = 1
+    _check(_run(lps, lens, tab, 1.5, env), lps, lens, tab, 1.5)
+
+
+@pytest.mark.parametrize("seq", ["0", "1", "2"])
+@pytest.mark.parametrize("regime", ["dense", "blank3", "clean"])
+def test_bench_regimes_vs_oracle(t20k, regime, seq):
+    from paper_2508_07014_b200.acoustic import synth_ctc_emissions
+    from paper_2508_07014_b200.context import Vocabulary
+
+    phrases, V, tab = t20k
+    rng = np.random.default_rng(33)
+    B, T = 32, 200
+    if regime == "clean":
+        vocab = Vocabulary(tokens=tuple(str(i) for i in range(V)), blank_id=0)
+        ems = []
+        for _ in range(B):
+            tgt = [int(x) for x in rng.integers(1, V, size=T // 4)]
+            em = synth_ctc_emissions(tgt, vocab, margin=0.5, seed=int(rng.integers(2**31)), boost_positions=[],
+                                     blanks_between=3)
+            ems.append(em.logprobs[:T])
+        T = min(e.shape[0] for e in ems)
+        lps = np.stack([e[:T] for e in ems]).astype(np.float32)
+    else:
+        logits = rng.normal(0.0, 2.0, size=(B, T, V))
+        if regime == "blank3":
+            logits[:, np.arange(T) % 4 != 0, 0] += 10.0
+        lps = gi.log_softmax(logits).astype(np.float32)
+    for lam in (0.0, 1.0):
+        _check(_run(lps, None, tab, lam, {"PGPB_CTC_SEQ": seq}), lps, None, tab, lam)
+
+
+def test_small_tree_unk_root_rows():
+    """100-phrase tree: most tokens have no root arc (root score = unk), so
+    the top-2 bound rarely certifies and the warp rescan path decides."""
+    phrases, V = gi.corpus("p100_v1024")
+    rng = np.random.default_rng(34)
+    for unk in (0.0, -0.5, 0.7):
+        tab = product_table(phrases, V, unk=unk)
+        lps = np.stack([gi.random_emissions(rng, 150, V) for _ in range(8)])
+        for lam in (0.7, 3.0):
+            _check(_run(lps, None, tab, lam), lps, None, tab, lam)
+
+
+@pytest.mark.parametrize("V", [1023, 37, 5])
+def test_vocab_not_multiple_of_four(V):
+    rng = np.random.default_rng(35 + V)
+    phrases = gi.random_phrase_set(rng, 60 if V > 40 else 12, 6, V)
+    tab = product_table(phrases, V)
+    B, T = 10, 300
+    lps = np.stack([_phrase_emissions(rng, phrases, T, V, noise=0.4) for _ in range(B)])
+    lens = rng.integers(0, T + 1, size=B).astype(np.int32)
+    for lam in (1.0, 4.0):
+        _check(_run(lps, lens, tab, lam), lps, lens, tab, lam)
+
+
+def test_fused_equals_two_phase(t20k):
+    """Same device outputs as the two-phase kernels (PGPB_CTC_TWOPHASE=1)."""
+    import torch
+
+    from paper_2508_07014_b200 import DecodeConfig, ctc_greedy_device
+
+    phrases, V, tab = t20k
+    g = torch.Generator(device="cuda")
+    g.manual_seed(36)
+    B, T = 96, 250
+    lp = torch.log_softmax(torch.randn((B, T, V), generator=g, device="cuda") * 2.0, dim=-1)
+    lens = torch.randint(0, T + 1, (B,), generator=g, device="cuda", dtype=torch.int32)
+    for lam in (0.0, 0.5, 1.0, 2.0):
+        cfg = DecodeConfig(lam=lam)
+        a = ctc_greedy_device(lp, lens, tab, cfg, 0)
+        os.environ["PGPB_CTC_TWOPHASE"] = "1"
+        try:
+            b = ctc_greedy_device(lp, lens, tab, cfg, 0)
+        finally:
+            os.environ.pop("PGPB_CTC_TWOPHASE")
+        torch.cuda.synchronize()
+        assert torch.equal(a.num_out, b.num_out)
+        assert torch.equal(a.am, b.am) and torch.equal(a.boost, b.boost)
+        for i in range(B):
+            n = int(a.num_out[i])
+            assert torch.equal(a.tokens[i, :n], b.tokens[i, :n])
+            assert torch.equal(a.deltas[i, :n], b.deltas[i, :n])
+            assert torch.equal(a.states[i, :n], b.states[i, :n])
+
+
+def test_empty_and_single_frame_batches(t20k):
+    phrases, V, tab = t20k
+    rng = np.random.default_rng(37)
+    lps = np.stack([gi.random_emissions(rng, 5, V) for _ in range(7)])
+    lens = np.array([0, 1, 0, 5, 2, 0, 1], dtype=np.int32)
+    _check(_run(lps, lens, tab, 1.0), lps, lens, tab, 1.0)
