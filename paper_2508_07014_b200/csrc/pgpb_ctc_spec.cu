@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(256) frame_top2_kernel(const float *__restrict
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const int64_t F = B * T;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t p = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; 2 * p < F; p += nwarps) {
     const int64_t f0 = 2 * p, f1 = 2 * p + 1;
     bool v0 = true, v1 = f1 < F;
@@ -758,6 +759,8 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
     for (int i = threadIdx.x; i < W * Vw; i += nthreads) s.bm[i] = 0u;
   }
   const int root_off = boost ? __ldg(t.blob_off) : 0;
+  // programmatic dependent launch: the prologue above overlaps phase A's tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   Ctx x;
   x.t = &t;
   x.s = &s;
@@ -772,7 +775,7 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
 
   for (int64_t b = blockIdx.x; b < g.B; b += gridDim.x) {
     const int64_t Tb = g.lengths ? int64_t(__ldg(g.lengths + b)) : g.T;
-    double am = 0.0, bo = 0.0;  // thread 0 only
+    double am = 0.0, bo = 0.0;  // warp 0: am (and boost when W == 1); warp 1: boost
     __syncthreads();
     if (threadIdx.x == 0) {
       s.misc[0] = root_off;
@@ -985,32 +988,37 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
       }
       __syncthreads();
       // ---- tail: ordered sums, compaction ----
-      if (threadIdx.x == 0) {
+      // am (warp 0) and boost (warp 1, or warp 0 when alone) are two
+      // independent fp64 chains in frame order, the reference's rounding
+      // sequence; each warp loads 32 frames at a time and walks them by
+      // shuffle (+ 0.0 for a frame without an emission is exact).
+      if ((wid == 0 || (wid == 1 && boost)) && lane == 0) {
 #ifdef PGPB_SEQ_PROFILE
         const long long t0 = clock64();
 #endif
+        const bool do_am = wid == 0, do_bo = boost && (wid == 1 || W == 1);
         int f = 0;
-        for (; f + 4 <= n; f += 4) {
-          float l4[4], s4[4];
-          int t4[4];
+        for (; f + 8 <= n; f += 8) {
+          float l8[8], s8[8];
+          int t8[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            l4[u] = s.o_lp[f + u];
-            t4[u] = s.o_tok[f + u];
-            s4[u] = boost ? s.o_s[f + u] : 0.0f;
+          for (int u = 0; u < 8; ++u) {
+            l8[u] = s.o_lp[f + u];
+            t8[u] = s.o_tok[f + u];
+            s8[u] = boost ? s.o_s[f + u] : 0.0f;
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {  // + 0.0 for frames without an emission is exact
-            am = __dadd_rn(am, static_cast<double>(l4[u]));
-            bo = __dadd_rn(bo, t4[u] >= 0 ? static_cast<double>(s4[u]) : 0.0);
+          for (int u = 0; u < 8; ++u) {
+            if (do_am) am = __dadd_rn(am, static_cast<double>(l8[u]));
+            if (do_bo) bo = __dadd_rn(bo, t8[u] >= 0 ? static_cast<double>(s8[u]) : 0.0);
           }
         }
         for (; f < n; ++f) {
-          am = __dadd_rn(am, static_cast<double>(s.o_lp[f]));
-          if (boost && s.o_tok[f] >= 0) bo = __dadd_rn(bo, static_cast<double>(s.o_s[f]));
+          if (do_am) am = __dadd_rn(am, static_cast<double>(s.o_lp[f]));
+          if (do_bo) bo = __dadd_rn(bo, s.o_tok[f] >= 0 ? static_cast<double>(s.o_s[f]) : 0.0);
         }
 #ifdef PGPB_SEQ_PROFILE
-        if (blockIdx.x == 0) CF_COUNT(13, clock64() - t0);
+        if (blockIdx.x == 0 && threadIdx.x == 0) CF_COUNT(13, clock64() - t0);
 #endif
       }
       // block exclusive scan of emit flags over n frames
@@ -1068,8 +1076,9 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
     if (threadIdx.x == 0) {
       g.nout[b] = s.misc[2];
       g.am_out[b] = am;
-      g.boost_out[b] = bo;
+      if (!boost || W == 1) g.boost_out[b] = bo;
     }
+    if (threadIdx.x == 32 && boost) g.boost_out[b] = bo;
   }
 }
 
@@ -1146,8 +1155,19 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctc_walk_kernel, 32 * W, smem);
   const int64_t cap = int64_t(sm_count(current_device())) * std::max(per_sm, 1);
   const unsigned grid = unsigned(B < cap ? B : cap);
-  ctc_walk_kernel<<<grid, 32 * W, smem, st>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32 * W);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  const char *epdl = getenv("PGPB_CTC_PDL");
+  cfg.attrs = attr;
+  cfg.numAttrs = (epdl && atoi(epdl) == 0) ? 0 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ctc_walk_kernel, a);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (top) cudaFreeAsync(top, st);
   if (e != cudaSuccess) return fail(PGPB_ECUDA, std::string("ctc_walk_kernel: ") + cudaGetErrorString(e));
   return PGPB_OK;
