@@ -12,8 +12,11 @@ launch over one resident batch of states; outputs rotate through a ring
 of 4 x 64 MiB buffers (256 MiB > 126 MB L2), so every step's writes reach
 HBM.  `e2e`: same metric through the public API with host numpy buffers
 (get_scores_batch: H2D states, kernel, D2H of both [B,V] outputs).
-`decode`: boosted vs unboosted fused greedy CTC RTFx (20K tree, V=1024,
-batch 128 x 200 frames of synthetic log-probs), device-timed.
+`decode_rnnt` (config 2), `decode_ctc` (greedy CTC per emission regime,
+"clean" = the reference's own decode-overhead corpus shape),
+`decode_device_beams` (configs 3 and 4, batched device beams) and
+`decode_beams` (per-utterance reference-API beams vs the CPU port):
+boosted vs unboosted, device-timed.
 `cpu_baseline`: the reference's own compiled kernel (oracle/_ref, built
 from /root/reference's _kernels.pyx) on the host cores, bounded sample.
 """
@@ -279,6 +282,8 @@ def run_ours(args, rank, world, local):
         out["boosted_decode_rtfx"] = out["decode_rnnt"]["boosted"]["rtfx"]
         out["decode_ctc"] = bench_decode(tab, V, dev, rank, world)
         out["gpu_launches"] += out["decode_ctc"].pop("_launches", 0)
+        out["decode_device_beams"] = bench_device_beams(dev, rank, world)
+        out["gpu_launches"] += out["decode_device_beams"].pop("_launches", 0)
     if rank == 0 and world == 1 and not args.no_decode:
         out["decode_beams"] = bench_beams()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -286,29 +291,55 @@ def run_ours(args, rank, world, local):
     return out
 
 
-def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
-    """Device-timed fused greedy CTC: boosted vs unboosted RTFx (audio = B*T*0.04 s).
+def _ctc_regimes(B, T, V, dev, rank):
+    """Synthetic emission regimes for the greedy CTC decode benchmark.
 
-    Two synthetic emission regimes: "dense" (log_softmax(N(0, 2)) rows, the
-    reference's random_emissions — almost every frame emits a token, the
-    worst case for the sequential rerank) and "blank3" (blank boosted by +10
-    nats on 3 of every 4 frames, the emitting-frame density of the
-    reference's own decode-overhead benchmark, tests/test_acceptance.py:346-353).
+    clean  : the reference's own decode-overhead corpus shape
+             (tests/test_acceptance.py:342-378): synth_ctc_emissions with
+             random targets, blanks_between=3, no boost positions, so
+             boosting must not change the output (peaky, blank-dominated).
+    blank3 : log_softmax(N(0, 2)) rows with the blank pushed up by 10 nats on
+             3 of every 4 frames (random, boost-sensitive emitting frames).
+    dense  : log_softmax(N(0, 2)) rows, the reference's random_emissions
+             (conftest.py:141-145): almost every frame emits and boosting
+             flips most decisions -- the sequential worst case.
     """
+    import torch
+
+    from paper_2508_07014_b200.acoustic import synth_ctc_emissions
+    from paper_2508_07014_b200.context import Vocabulary
+
+    rng = np.random.default_rng(4242 + rank)
+    vocab = Vocabulary(tokens=tuple(str(i) for i in range(V)), blank_id=0)
+    ems = []
+    for _ in range(B):
+        tgt = [int(x) for x in rng.integers(1, V, size=T // 4 + 1)]
+        ems.append(synth_ctc_emissions(tgt, vocab, margin=0.5, seed=int(rng.integers(2**31)), boost_positions=[],
+                                       blanks_between=3).logprobs[:T])
+    yield "clean", torch.from_numpy(np.stack(ems)).to(dev)
+    del ems
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    logits = torch.randn((B, T, V), generator=g, device=dev) * 2.0
+    lp = torch.log_softmax(logits, dim=-1)
+    yield "dense", lp
+    del lp
+    logits[:, torch.arange(T, device=dev) % 4 != 0, 0] += 10.0
+    yield "blank3", torch.log_softmax(logits, dim=-1)
+
+
+def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
+    """Device-timed fused greedy CTC (phase A top-2 + speculative walker):
+    boosted vs unboosted RTFx (audio = B*T*0.04 s) per emission regime."""
     import torch
 
     import paper_2508_07014_b200 as pb
 
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-    out = {"workload": f"fused greedy CTC, batch {B} x {T} frames, V={V}, 20K-phrase tree, lam=1 vs lam=0"}
+    out = {"workload": f"greedy CTC, batch {B} x {T} frames, V={V}, 20K-phrase tree, lam=1 vs lam=0",
+           "headline_regime": "clean"}
     launches = 0
-    for regime in ("dense", "blank3"):
-        logits = torch.randn((B, T, V), generator=g, device=dev) * 2.0
-        if regime == "blank3":
-            logits[:, torch.arange(T, device=dev) % 4 != 0, 0] += 10.0
-        lp = torch.log_softmax(logits, dim=-1).contiguous()
-        del logits
+    for regime, lp in _ctc_regimes(B, T, V, dev, rank):
+        lp = lp.contiguous()
         res = {}
         for name, cfg in (("unboosted", pb.DecodeConfig(lam=0.0)), ("boosted", pb.DecodeConfig(lam=1.0))):
             o = pb.ctc_greedy_device(lp, None, tab, cfg, 0)
@@ -326,12 +357,87 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
             torch.cuda.synchronize(dev)
             launches += 2 * reps
             ms = s.elapsed_time(e) / reps
-            res[name] = {"ms": ms, "rtfx": B * T * FRAME_SEC / (ms / 1e3) * world}
+            res[name] = {"ms": ms, "rtfx": B * T * FRAME_SEC / (ms / 1e3) * world,
+                         "hbm_gbs": B * T * V * 4 / (ms / 1e3) / 1e9}
             if name == "boosted":
                 res["emitted_per_utt"] = float(o.num_out.double().mean().item())
         res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
         out[regime] = res
         del lp
+    out["_launches"] = launches
+    return out
+
+
+def bench_device_beams(dev, rank, world):
+    """Configs 3 and 4 as batched device-resident beam searches (beams.py):
+    config 3 = RNN-T beam 4, 5K-phrase tree, V=1024, batch 64 x 200 frames,
+    random-init stateless prediction net + joint (bf16 GEMMs), max 5 symbols
+    per frame, one pgpb_tbeam_wave launch per wave, a frame replayed as a CUDA
+    graph; config 4 = AED beam 4, 20K-phrase tree, V=4096, batch 64, max_len
+    48, random-init 4-layer transformer decoder (d=256, FF 1024), one
+    pgpb_aed_step launch per token step.  Boosted (lam=1) vs unboosted
+    (lam=0), device time of one whole batch decode."""
+    import torch
+
+    import gen_inputs as gi
+    import paper_2508_07014_b200 as pb
+    from paper_2508_07014_b200.beams import (AEDBeamDecoder, StatelessTransducerModel, TransducerBeamDecoder,
+                                             TransformerAEDModel)
+
+    def table(name):
+        phrases, V = gi.corpus(name)
+        ctx = pb.ContextList([pb.Phrase(" ".join(map(str, p)), p) for p in phrases], min_chars=0)
+        return pb.compile_arc_table(pb.compute_fail_links(pb.build_prefix_tree(ctx, pb.TreeParams(), V))), V
+
+    def timed(fn, n=3):
+        fn()
+        ts = []
+        for _ in range(n):
+            torch.cuda.synchronize(dev)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize(dev)
+            ts.append(s.elapsed_time(e))
+        return statistics.median(ts)
+
+    out = {}
+    launches = 0
+    tab5, V = table("p5k_v1024")
+    B, T, D = 64, 200, 512
+    model = StatelessTransducerModel(V, enc_dim=D, pred_dim=640, joint_dim=640, seed=3 + rank, blank_bias=4.0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77 + rank)
+    enc = model.project_encoder(torch.randn((B, T, D), generator=g, device=dev))
+    res = {"workload": f"RNN-T beam 4, batch {B} x {T} frames, V={V}, 5K-phrase tree, stateless pred net + joint, "
+                       "max 5 symbols/frame"}
+    for name, lam in (("unboosted", 0.0), ("boosted", 1.0)):
+        dec = TransducerBeamDecoder(model, tab5, pb.DecodeConfig(lam=lam, beam_size=4, max_symbols_per_frame=5), B, T)
+        ms = timed(lambda: dec.run(enc))
+        launches += 4 * dec.launches
+        best = dec.results()
+        res[name] = {"ms": ms, "rtfx": B * T * FRAME_SEC / (ms / 1e3) * world, "waves": dec.launches,
+                     "best_len_mean": float(np.mean([len(nb[0].tokens) if nb else 0 for nb in best]))}
+    res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
+    out["config3_rnnt_beam"] = res
+    del dec, model, enc
+    tab20, V4 = table("p20k_v4096")
+    B, Tm, max_len = 64, 100, 48
+    model = TransformerAEDModel(V4, d_model=256, n_layers=4, n_heads=4, d_ff=1024, max_len=max_len + 1,
+                                seed=5 + rank)
+    mem = torch.randn((B, Tm, 256), generator=g, device=dev)
+    res = {"workload": f"AED beam 4, batch {B}, V={V4}, 20K-phrase tree, 4-layer transformer decoder d=256, "
+                       f"max_len {max_len}, eos bump on"}
+    for name, lam in (("unboosted", 0.0), ("boosted", 1.0)):
+        dec = AEDBeamDecoder(model, tab20, pb.DecodeConfig(lam=lam, beam_size=4), B, max_len=max_len, eos=V4 - 1)
+        ms = timed(lambda: dec.run(mem))
+        launches += 4 * dec.launches
+        best = dec.results()
+        toks = float(np.mean([len(nb[0].tokens) if nb else 0 for nb in best]))
+        res[name] = {"ms": ms, "utt_per_s": B / (ms / 1e3) * world, "steps": dec.launches, "best_len_mean": toks}
+    res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
+    out["config4_aed_beam"] = res
     out["_launches"] = launches
     return out
 
