@@ -857,8 +857,8 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
           // the two most recent argmax emissions v1, v2 (in that order)
           int v1 = -1, v2 = -1;
           const int lim = max(0, cb - 64);
-          for (int t = cb - 1; t >= lim && v1 < 0; --t) {
-            const int at = s.fa[t], ap = t ? s.fa[t - 1] : s.misc[1];
+          for (int u = cb - 1; u >= lim && v1 < 0; --u) {
+            const int at = s.fa[u], ap = u ? s.fa[u - 1] : s.misc[1];
             if (at != g.blank && at != ap) {
               if (v2 < 0)
                 v2 = at;
