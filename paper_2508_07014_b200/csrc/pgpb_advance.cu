@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kThreads)
 // current row streams out.  Requires V % 4 == 0 and smem root staging.
 __global__ void __launch_bounds__(kThreads, 3)
     advance_v5_kernel(TableView t, const int32_t *__restrict__ states, int64_t B,
-                      float *__restrict__ scores, int32_t *__restrict__ next, int rows_per_cta) {
+                      float *__restrict__ scores, int32_t *__restrict__ next, int rows_per_cta, int split) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int V = t.vocab_size, Vp = t.vocab_padded, Vw = (V + 31) >> 5;
   const int64_t r0 = int64_t(blockIdx.x) * rows_per_cta;
@@ -344,33 +344,44 @@ __global__ void __launch_bounds__(kThreads, 3)
   float *ovs = reinterpret_cast<float *>(wb);
   int32_t *ovn = reinterpret_cast<int32_t *>(wb + size_t(Vp) * 4);
   unsigned *bm = reinterpret_cast<unsigned *>(wb + size_t(Vp) * 8);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s_rec[i] = __ldg(t.clo_rec + __ldg(states + r0 + i));
+  // table-only prologue first; with programmatic dependent launch it overlaps
+  // the previous kernel's tail, and the states are read after the wait
   stage_root(t, s_root, s_next);
   for (int w = lane; w < Vw; w += 32) bm[w] = 0u;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_rec[i] = __ldg(t.clo_rec + __ldg(states + r0 + i));
   __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const float4 *r4 = reinterpret_cast<const float4 *>(s_root);
   const int4 *q4 = reinterpret_cast<const int4 *>(s_next);
   const int V4 = V >> 2;
-  int j = wib;
-  int4 rec = j < n ? s_rec[j] : make_int4(0, 0, 0, 0);
+  // Work unit = (row, column part): rows split into `split` parts balance
+  // the warps when a CTA's row count is not a multiple of its warp count.
+  const int W = blockDim.x >> 5, nu = n * split;
+  int u = wib;
+  int j = u / split, q = u - j * split;
+  int4 rec = u < nu ? s_rec[j] : make_int4(0, 0, 0, 0);
   int4 e = (lane < rec.y) ? __ldg(t.clo + rec.x + lane) : make_int4(0, 0, 0, 0);
-  const int W = blockDim.x >> 5;
-  for (; j < n; j += W) {
-    // overrides of this row -> scratch + bitmap
-    if (lane < rec.y) {
+  for (; u < nu; u += W) {
+    const int c0 = (V4 * q) / split, c1 = (V4 * (q + 1)) / split;
+    const int v0 = 4 * c0, v1 = 4 * c1;
+    // overrides of this part -> scratch + bitmap
+    if (lane < rec.y && e.x >= v0 && e.x < v1) {
       ovs[e.x] = __int_as_float(e.z);
       ovn[e.x] = e.y;
       atomicOr(bm + (e.x >> 5), 1u << (e.x & 31));
     }
     for (int i = lane + 32; i < rec.y; i += 32) {
       const int4 e2 = __ldg(t.clo + rec.x + i);
+      if (e2.x < v0 || e2.x >= v1) continue;
       ovs[e2.x] = __int_as_float(e2.z);
       ovn[e2.x] = e2.y;
       atomicOr(bm + (e2.x >> 5), 1u << (e2.x & 31));
     }
-    // prefetch the next row's record and first closure entries
-    const int jn = j + W;
-    const int4 nrec = jn < n ? s_rec[jn] : make_int4(0, 0, 0, 0);
+    // prefetch the next unit's record and first closure entries
+    const int un = u + W;
+    const int jn = un / split, qn = un - jn * split;
+    const int4 nrec = un < nu ? s_rec[jn] : make_int4(0, 0, 0, 0);
     const int4 ne = (lane < nrec.y) ? __ldg(t.clo + nrec.x + lane) : make_int4(0, 0, 0, 0);
     __syncwarp();
     const float acc = __int_as_float(rec.z);
@@ -378,9 +389,9 @@ __global__ void __launch_bounds__(kThreads, 3)
     float4 *s4 = reinterpret_cast<float4 *>(scores + row * V);
     int4 *n4 = reinterpret_cast<int4 *>(next + row * V);
 #pragma unroll 4
-    for (int c = lane; c < V4; c += 32) {
+    for (int c = c0 + lane; c < c1; c += 32) {
       float4 r = r4[c];
-      int4 q = q4[c];
+      int4 qv = q4[c];
       r.x = acc + r.x;
       r.y = acc + r.y;
       r.z = acc + r.z;
@@ -388,13 +399,114 @@ __global__ void __launch_bounds__(kThreads, 3)
       const unsigned bits = (bm[c >> 3] >> ((c & 7) * 4)) & 0xFu;
       if (bits) {
         const int v = 4 * c;
-        if (bits & 1u) { r.x = ovs[v]; q.x = ovn[v]; }
-        if (bits & 2u) { r.y = ovs[v + 1]; q.y = ovn[v + 1]; }
-        if (bits & 4u) { r.z = ovs[v + 2]; q.z = ovn[v + 2]; }
-        if (bits & 8u) { r.w = ovs[v + 3]; q.w = ovn[v + 3]; }
+        if (bits & 1u) { r.x = ovs[v]; qv.x = ovn[v]; }
+        if (bits & 2u) { r.y = ovs[v + 1]; qv.y = ovn[v + 1]; }
+        if (bits & 4u) { r.z = ovs[v + 2]; qv.z = ovn[v + 2]; }
+        if (bits & 8u) { r.w = ovs[v + 3]; qv.w = ovn[v + 3]; }
       }
       __stcs(s4 + c, r);
-      __stcs(n4 + c, q);
+      __stcs(n4 + c, qv);
+    }
+    __syncwarp();
+    for (int w = (v0 >> 5) + lane; w < ((v1 + 31) >> 5); w += 32) bm[w] = 0u;
+    __syncwarp();
+    rec = nrec;
+    e = ne;
+    j = jn;
+    q = qn;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// v6: v5 without the per-warp scratch row.  A row's closure arcs are sorted
+// by token, so the arc overriding token v is the rank(v)-th one: per row the
+// warp sets the arcs' bits in a bitmap and takes an exclusive prefix
+// popcount over its words; the streaming pass finds each override's arc
+// (an L1 hit: the row's arcs were just loaded) by rank.  Shared memory per
+// warp drops from V*8 B to Vw*8 B, so more CTAs fit per SM.
+__global__ void __launch_bounds__(kThreads, 4)
+    advance_v6_kernel(TableView t, const int32_t *__restrict__ states, int64_t B,
+                      float *__restrict__ scores, int32_t *__restrict__ next, int rows_per_cta) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int V = t.vocab_size, Vp = t.vocab_padded, Vw = (V + 31) >> 5;
+  const int64_t r0 = int64_t(blockIdx.x) * rows_per_cta;
+  const int n = static_cast<int>(min(int64_t(rows_per_cta), B - r0));
+  const size_t rec_bytes = (size_t(rows_per_cta) * 16 + 255) & ~size_t(255);
+  int4 *s_rec = reinterpret_cast<int4 *>(smem);
+  float *s_root = reinterpret_cast<float *>(smem + rec_bytes);
+  int32_t *s_next = reinterpret_cast<int32_t *>(smem + rec_bytes + size_t(Vp) * 4);
+  const size_t wbytes = (size_t(Vw) * 8 + 15) & ~size_t(15);
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned *bm = reinterpret_cast<unsigned *>(smem + rec_bytes + size_t(Vp) * 8 + size_t(wib) * wbytes);
+  int *pre = reinterpret_cast<int *>(bm + Vw);
+  stage_root(t, s_root, s_next);
+  for (int w = lane; w < Vw; w += 32) bm[w] = 0u;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_rec[i] = __ldg(t.clo_rec + __ldg(states + r0 + i));
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const float4 *r4 = reinterpret_cast<const float4 *>(s_root);
+  const int4 *q4 = reinterpret_cast<const int4 *>(s_next);
+  const int V4 = V >> 2;
+  const int W = blockDim.x >> 5;
+  int j = wib;
+  int4 rec = j < n ? s_rec[j] : make_int4(0, 0, 0, 0);
+  int4 e = (lane < rec.y) ? __ldg(t.clo + rec.x + lane) : make_int4(0, 0, 0, 0);
+  for (; j < n; j += W) {
+    if (lane < rec.y) atomicOr(bm + (e.x >> 5), 1u << (e.x & 31));
+    for (int i = lane + 32; i < rec.y; i += 32) {
+      const int tok = __ldg(&t.clo[rec.x + i].x);
+      atomicOr(bm + (tok >> 5), 1u << (tok & 31));
+    }
+    const int jn = j + W;
+    const int4 nrec = jn < n ? s_rec[jn] : make_int4(0, 0, 0, 0);
+    const int4 ne = (lane < nrec.y) ? __ldg(t.clo + nrec.x + lane) : make_int4(0, 0, 0, 0);
+    __syncwarp();
+    // exclusive prefix popcount over the bitmap words (lane-contiguous words)
+    {
+      const int per = (Vw + 31) >> 5, w0 = lane * per;
+      int cnt = 0;
+      for (int k = 0; k < per; ++k)
+        if (w0 + k < Vw) cnt += __popc(bm[w0 + k]);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - cnt;
+      for (int k = 0; k < per; ++k)
+        if (w0 + k < Vw) {
+          pre[w0 + k] = run;
+          run += __popc(bm[w0 + k]);
+        }
+    }
+    __syncwarp();
+    const float acc = __int_as_float(rec.z);
+    const int64_t row = r0 + j;
+    float4 *s4 = reinterpret_cast<float4 *>(scores + row * V);
+    int4 *n4 = reinterpret_cast<int4 *>(next + row * V);
+    const int4 *arcs = t.clo + rec.x;
+#pragma unroll 4
+    for (int c = lane; c < V4; c += 32) {
+      float4 r = r4[c];
+      int4 qv = q4[c];
+      r.x = acc + r.x;
+      r.y = acc + r.y;
+      r.z = acc + r.z;
+      r.w = acc + r.w;
+      const unsigned word = bm[c >> 3];
+      const int sh = (c & 7) * 4;
+      const unsigned bits = (word >> sh) & 0xFu;
+      if (bits) {
+        int k = pre[c >> 3] + __popc(word & ((1u << sh) - 1u));
+        if (bits & 1u) { const int4 a = __ldg(arcs + k++); r.x = __int_as_float(a.z); qv.x = a.y; }
+        if (bits & 2u) { const int4 a = __ldg(arcs + k++); r.y = __int_as_float(a.z); qv.y = a.y; }
+        if (bits & 4u) { const int4 a = __ldg(arcs + k++); r.z = __int_as_float(a.z); qv.z = a.y; }
+        if (bits & 8u) { const int4 a = __ldg(arcs + k); r.w = __int_as_float(a.z); qv.w = a.y; }
+      }
+      __stcs(s4 + c, r);
+      __stcs(n4 + c, qv);
     }
     __syncwarp();
     for (int w = lane; w < Vw; w += 32) bm[w] = 0u;
@@ -404,14 +516,96 @@ __global__ void __launch_bounds__(kThreads, 3)
   }
 }
 
-static int g_variant = -1;
+
+// ---------------------------------------------------------------------------
+// v7: one warp per CTA and `rows_per_cta` rows each, so the block scheduler
+// balances rows across SMs dynamically (no static rows-per-warp imbalance);
+// the dense root row is read through L1 (__ldg: 8 KB per SM, every CTA on
+// the SM hits it), overrides by bitmap rank as in v6.
+__global__ void __launch_bounds__(32)
+    advance_v7_kernel(TableView t, const int32_t *__restrict__ states, int64_t B,
+                      float *__restrict__ scores, int32_t *__restrict__ next, int rows_per_cta) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int V = t.vocab_size, Vw = (V + 31) >> 5;
+  const int lane = threadIdx.x;
+  unsigned *bm = reinterpret_cast<unsigned *>(smem);
+  int *pre = reinterpret_cast<int *>(bm + Vw);
+  for (int w = lane; w < Vw; w += 32) bm[w] = 0u;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t r0 = int64_t(blockIdx.x) * rows_per_cta;
+  const int n = static_cast<int>(min(int64_t(rows_per_cta), B - r0));
+  const float4 *r4 = reinterpret_cast<const float4 *>(t.root_scores);
+  const int4 *q4 = reinterpret_cast<const int4 *>(t.root_next);
+  const int V4 = V >> 2;
+  int4 rec = n > 0 ? __ldg(t.clo_rec + __ldg(states + r0)) : make_int4(0, 0, 0, 0);
+  int4 e = (lane < rec.y) ? __ldg(t.clo + rec.x + lane) : make_int4(0, 0, 0, 0);
+  __syncwarp();
+  for (int j = 0; j < n; ++j) {
+    if (j == n - 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (lane < rec.y) atomicOr(bm + (e.x >> 5), 1u << (e.x & 31));
+    for (int i = lane + 32; i < rec.y; i += 32) {
+      const int tok = __ldg(&t.clo[rec.x + i].x);
+      atomicOr(bm + (tok >> 5), 1u << (tok & 31));
+    }
+    const int4 nrec = j + 1 < n ? __ldg(t.clo_rec + __ldg(states + r0 + j + 1)) : make_int4(0, 0, 0, 0);
+    const int4 ne = (lane < nrec.y) ? __ldg(t.clo + nrec.x + lane) : make_int4(0, 0, 0, 0);
+    __syncwarp();
+    {
+      const int per = (Vw + 31) >> 5, w0 = lane * per;
+      int cnt = 0;
+      for (int k = 0; k < per; ++k)
+        if (w0 + k < Vw) cnt += __popc(bm[w0 + k]);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - cnt;
+      for (int k = 0; k < per; ++k)
+        if (w0 + k < Vw) {
+          pre[w0 + k] = run;
+          run += __popc(bm[w0 + k]);
+        }
+    }
+    __syncwarp();
+    const float acc = __int_as_float(rec.z);
+    const int64_t row = r0 + j;
+    float4 *s4 = reinterpret_cast<float4 *>(scores + row * V);
+    int4 *n4 = reinterpret_cast<int4 *>(next + row * V);
+    const int4 *arcs = t.clo + rec.x;
+#pragma unroll 4
+    for (int c = lane; c < V4; c += 32) {
+      float4 r = __ldg(r4 + c);
+      int4 qv = __ldg(q4 + c);
+      r.x = acc + r.x;
+      r.y = acc + r.y;
+      r.z = acc + r.z;
+      r.w = acc + r.w;
+      const unsigned word = bm[c >> 3];
+      const int sh = (c & 7) * 4;
+      const unsigned bits = (word >> sh) & 0xFu;
+      if (bits) {
+        int k = pre[c >> 3] + __popc(word & ((1u << sh) - 1u));
+        if (bits & 1u) { const int4 a = __ldg(arcs + k++); r.x = __int_as_float(a.z); qv.x = a.y; }
+        if (bits & 2u) { const int4 a = __ldg(arcs + k++); r.y = __int_as_float(a.z); qv.y = a.y; }
+        if (bits & 4u) { const int4 a = __ldg(arcs + k++); r.z = __int_as_float(a.z); qv.z = a.y; }
+        if (bits & 8u) { const int4 a = __ldg(arcs + k); r.w = __int_as_float(a.z); qv.w = a.y; }
+      }
+      __stcs(s4 + c, r);
+      __stcs(n4 + c, qv);
+    }
+    __syncwarp();
+    for (int w = lane; w < Vw; w += 32) bm[w] = 0u;
+    __syncwarp();
+    rec = nrec;
+    e = ne;
+  }
+}
 
 static int advance_variant() {
-  if (g_variant < 0) {
-    const char *e = getenv("PGPB_ADVANCE_VARIANT");
-    g_variant = e ? atoi(e) : 5;
-  }
-  return g_variant;
+  const char *e = getenv("PGPB_ADVANCE_VARIANT");
+  return e ? atoi(e) : 6;
 }
 
 using AdvFn = void (*)(TableView, const int32_t *, int64_t, float *, int32_t *);
@@ -430,7 +624,59 @@ static int launch_advance(const pgpb_table *table, const int32_t *d_states, int6
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nsm = sm_count(current_device());
   const int variant = chain ? 1 : advance_variant();
-  if (variant == 5 && vec && smem_root) {
+  if (variant == 6 && vec && smem_root) {
+    const int Vw = (t.vocab_size + 31) >> 5;
+    const size_t wbytes = (size_t(Vw) * 8 + 15) & ~size_t(15);
+    const char *e = getenv("PGPB_V6_CTAS");
+    const int per_sm = e ? std::max(1, atoi(e)) : 4;
+    int64_t ctas = int64_t(nsm) * per_sm;
+    int rows = int((B + ctas - 1) / ctas);
+    if (rows < 1) rows = 1;
+    ctas = (B + rows - 1) / rows;
+    const size_t rec_bytes = (size_t(rows) * 16 + 255) & ~size_t(255);
+    const size_t smem6 = rec_bytes + root_bytes + size_t(kWarpsPerBlock) * wbytes;
+    if (smem6 <= 200 * 1024) {
+      if (smem6 > 48 * 1024)
+        PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(advance_v6_kernel),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem6)));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(unsigned(ctas));
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem6;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      const char *epdl = getenv("PGPB_ADVANCE_PDL");
+      cfg.attrs = attr;
+      cfg.numAttrs = (epdl && atoi(epdl) == 0) ? 0 : 1;
+      PGPB_CUDA_TRY(cudaLaunchKernelEx(&cfg, advance_v6_kernel, t, d_states, B, d_scores, d_next, rows));
+      PGPB_CUDA_TRY(cudaGetLastError());
+      return PGPB_OK;
+    }
+  }
+  if (variant == 7 && vec) {
+    const int Vw = (t.vocab_size + 31) >> 5;
+    const char *e = getenv("PGPB_V7_ROWS");
+    const int rows = e ? std::max(1, atoi(e)) : 2;
+    const int64_t ctas = (B + rows - 1) / rows;
+    const size_t smem7 = size_t(Vw) * 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(ctas));
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = smem7;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    const char *epdl = getenv("PGPB_ADVANCE_PDL");
+    cfg.attrs = attr;
+    cfg.numAttrs = (epdl && atoi(epdl) == 0) ? 0 : 1;
+    PGPB_CUDA_TRY(cudaLaunchKernelEx(&cfg, advance_v7_kernel, t, d_states, B, d_scores, d_next, rows));
+    PGPB_CUDA_TRY(cudaGetLastError());
+    return PGPB_OK;
+  }
+  if ((variant == 5 || variant == 6) && vec && smem_root) {
     const int Vw = (t.vocab_size + 31) >> 5;
     const size_t wbytes = size_t(t.vocab_padded) * 8 + ((size_t(Vw) * 4 + 15) & ~size_t(15));
     const char *e = getenv("PGPB_V5_CTAS");
@@ -446,7 +692,21 @@ static int launch_advance(const pgpb_table *table, const int32_t *d_states, int6
       if (smem5 * per_sm <= 224 * 1024 || (per_sm == 1 && smem5 <= 224 * 1024)) {
         PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(advance_v5_kernel),
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem5)));
-        advance_v5_kernel<<<unsigned(ctas), 32 * W, smem5, st>>>(t, d_states, B, d_scores, d_next, rows);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(ctas));
+        cfg.blockDim = dim3(32 * W);
+        cfg.dynamicSmemBytes = smem5;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        const char *epdl = getenv("PGPB_ADVANCE_PDL");
+        cfg.attrs = attr;
+        cfg.numAttrs = (epdl && atoi(epdl) == 0) ? 0 : 1;
+        // column parts per row: balance rows over the W warps of a CTA
+        int split = 1;  // column parts per row (measured: 1 is fastest at 8192 x 1024)
+        if (const char *es = getenv("PGPB_V5_SPLIT")) split = std::max(1, atoi(es));
+        PGPB_CUDA_TRY(cudaLaunchKernelEx(&cfg, advance_v5_kernel, t, d_states, B, d_scores, d_next, rows, split));
         PGPB_CUDA_TRY(cudaGetLastError());
         return PGPB_OK;
       }

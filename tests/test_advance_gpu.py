@@ -63,12 +63,17 @@ def test_advance_corpora_match_reference_golden(name):
     assert np.array_equal(c.next_states.cpu().numpy(), res.next_states)
 
 
-@pytest.mark.parametrize("name,B", [("p20k_v1024", 8192), ("p20k_v4096", 2048), ("p5k_v1024", 3000)])
-def test_advance_full_size_vs_oracle(name, B):
+@pytest.mark.parametrize("variant", ["6", "7", "5", "3", "2", "1"])
+@pytest.mark.parametrize("name,B", [("p20k_v1024", 8192), ("p20k_v4096", 2048), ("p5k_v1024", 3000),
+                                    ("p20k_v1024", 37)])
+def test_advance_full_size_vs_oracle(name, B, variant, monkeypatch):
+    """Every advance kernel variant (PGPB_ADVANCE_VARIANT; 6 is the default)
+    bit-exact against the oracle."""
     import torch
 
     from paper_2508_07014_b200 import get_scores_batch
 
+    monkeypatch.setenv("PGPB_ADVANCE_VARIANT", variant)
     phrases, V = gi.corpus(name)
     tab = product_table(phrases, V)
     rng = np.random.default_rng(B)
