@@ -267,7 +267,7 @@ def run_ours(args, rank, world, local):
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": ncu_traffic(), "peak_kind": peak_kind,
-                     "kernel": "advance_v5_kernel", "bytes_alg_per_launch": bytes_alg,
+                     "kernel": "advance_v6_kernel", "bytes_alg_per_launch": bytes_alg,
                      "kernel_ms": kern_ms,
                      "timing": "CUDA events around one graph replay of the K back-to-back launches"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": B * V * 8,
