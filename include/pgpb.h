@@ -113,6 +113,14 @@ int pgpb_table_create(int32_t num_states, int32_t vocab_size, int32_t num_arcs,
                       const float *h_backoff_weight, const uint8_t *h_is_final,
                       const float *h_final_score, float unk_score, int32_t device,
                       pgpb_table **out);
+/* GPB1 bytes (the reference's serialized table, table.py:16-29 / save_table
+ * :250-264) straight to a device table: parse + the reference's validate
+ * invariants (table.py:87-127) on the host, then pgpb_table_create.
+ * Replaces load_table (table.py:267-310) + the Python ArcTable for callers
+ * that only need the device table.  PGPB_EFORMAT on a malformed file.     */
+int pgpb_table_load_gpb1(const void *data, int64_t size, int32_t device, pgpb_table **out);
+int pgpb_table_load_gpb1_file(const char *path, int32_t device, pgpb_table **out);
+
 int pgpb_table_info_get(const pgpb_table *table, pgpb_table_info *out);
 void pgpb_table_destroy(pgpb_table *table);
 

@@ -88,6 +88,8 @@ _SIGS = {
     "pgpb_table_create": [c_int32, c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_float,
                           c_int32, POINTER(c_void_p)],
     "pgpb_table_info_get": [c_void_p, POINTER(TableInfo)],
+    "pgpb_table_load_gpb1": [_P, c_int64, c_int32, POINTER(c_void_p)],
+    "pgpb_table_load_gpb1_file": [ctypes.c_char_p, c_int32, POINTER(c_void_p)],
     "pgpb_advance": [c_void_p, _P, c_int64, _P, _P, c_void_p],
     "pgpb_advance_host": [c_void_p, _P, c_int64, _P, _P, c_void_p],
     "pgpb_advance_chain": [c_void_p, _P, c_int64, _P, _P, c_void_p],

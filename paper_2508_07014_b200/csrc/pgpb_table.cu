@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -242,6 +243,98 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   v.bits_words = Vw;
   *out = t;
   return PGPB_OK;
+}
+
+// GPB1 (table.py:16-29 of the reference; little-endian): header
+// "<4sIIIIf" = magic, version=1, S, V, A, unk_score, then arc_from,
+// arc_token, arc_to (i32[A]), arc_weight (f32[A]), state_start, state_end,
+// backoff_to (i32[S]), backoff_weight (f32[S]), is_final (u8[S]),
+// final_score (f32[S]).  Parsed and validated on the host (the reference's
+// ArcTable.validate invariants, table.py:87-127), then the device arena is
+// built directly: no intermediate Python arrays.
+int pgpb_table_load_gpb1(const void *data, int64_t size, int32_t device, pgpb_table **out) {
+  using pgpb::fail;
+  if (!out) return fail(PGPB_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!data && size) return fail(PGPB_EINVAL, "data is NULL");
+  const unsigned char *b = static_cast<const unsigned char *>(data);
+  const int64_t hdr = 24;
+  if (size < hdr) return fail(PGPB_EFORMAT, "truncated header");
+  if (std::memcmp(b, "GPB1", 4) != 0) return fail(PGPB_EFORMAT, "bad magic");
+  uint32_t version, S, V, A;
+  float unk;
+  std::memcpy(&version, b + 4, 4);
+  std::memcpy(&S, b + 8, 4);
+  std::memcpy(&V, b + 12, 4);
+  std::memcpy(&A, b + 16, 4);
+  std::memcpy(&unk, b + 20, 4);
+  if (version != 1) return fail(PGPB_EFORMAT, "unsupported version " + std::to_string(version));
+  if (S > uint32_t(INT32_MAX) || V > uint32_t(INT32_MAX) || A > uint32_t(INT32_MAX))
+    return fail(PGPB_EFORMAT, "counts exceed int32");
+  const int64_t expected = hdr + int64_t(A) * 16 + int64_t(S) * 21;
+  if (size != expected)
+    return fail(PGPB_EFORMAT, "expected " + std::to_string(expected) + " bytes, found " + std::to_string(size));
+  // copy out (the arrays are unaligned inside the file)
+  int64_t off = hdr;
+  auto take_i32 = [&](int64_t n) {
+    std::vector<int32_t> v(static_cast<size_t>(n));
+    if (n) std::memcpy(v.data(), b + off, size_t(n) * 4);
+    off += n * 4;
+    return v;
+  };
+  auto take_f32 = [&](int64_t n) {
+    std::vector<float> v(static_cast<size_t>(n));
+    if (n) std::memcpy(v.data(), b + off, size_t(n) * 4);
+    off += n * 4;
+    return v;
+  };
+  const std::vector<int32_t> arc_from = take_i32(A), arc_token = take_i32(A), arc_to = take_i32(A);
+  const std::vector<float> arc_weight = take_f32(A);
+  const std::vector<int32_t> state_start = take_i32(S), state_end = take_i32(S), backoff_to = take_i32(S);
+  const std::vector<float> backoff_weight = take_f32(S);
+  std::vector<uint8_t> is_final(static_cast<size_t>(S));
+  if (S) std::memcpy(is_final.data(), b + off, S);
+  off += S;
+  const std::vector<float> final_score = take_f32(S);
+  // ArcTable.validate (table.py:87-127): shapes, ranges, sort order, arc
+  // ranges consistent with arc_from, the root's backoff, finals
+  if (S < 1) return fail(PGPB_EFORMAT, "need at least the root state");
+  for (uint32_t j = 0; j < A; ++j) {
+    if (arc_from[j] < 0 || uint32_t(arc_from[j]) >= S) return fail(PGPB_EFORMAT, "arc_from out of range");
+    if (arc_token[j] < 0 || uint32_t(arc_token[j]) >= V) return fail(PGPB_EFORMAT, "arc_token out of range");
+    if (arc_to[j] < 0 || uint32_t(arc_to[j]) >= S) return fail(PGPB_EFORMAT, "arc_to out of range");
+    if (!std::isfinite(arc_weight[j])) return fail(PGPB_EFORMAT, "non-finite arc weight");
+    if (j && (arc_from[j] < arc_from[j - 1] || (arc_from[j] == arc_from[j - 1] && arc_token[j] <= arc_token[j - 1])))
+      return fail(PGPB_EFORMAT, "arcs not strictly sorted by (from, token)");
+  }
+  for (uint32_t st = 0; st < S; ++st) {
+    if (state_start[st] < 0 || state_start[st] > state_end[st] || uint32_t(state_end[st]) > A)
+      return fail(PGPB_EFORMAT, "state " + std::to_string(st) + ": bad arc range");
+    for (int32_t j = state_start[st]; j < state_end[st]; ++j)
+      if (uint32_t(arc_from[j]) != st) return fail(PGPB_EFORMAT, "arc range inconsistent with arc_from");
+    if (is_final[st] > 1) return fail(PGPB_EFORMAT, "is_final must be 0/1");
+    if (!std::isfinite(backoff_weight[st]) || !std::isfinite(final_score[st]))
+      return fail(PGPB_EFORMAT, "non-finite state score");
+  }
+  if (backoff_to[0] != 0 || backoff_weight[0] != 0.0f) return fail(PGPB_EFORMAT, "root backoff must be (0, 0)");
+  return pgpb_table_create(int32_t(S), int32_t(V), int32_t(A), arc_token.data(), arc_to.data(), arc_weight.data(),
+                           state_start.data(), state_end.data(), backoff_to.data(), backoff_weight.data(),
+                           is_final.data(), final_score.data(), unk, device, out);
+}
+
+int pgpb_table_load_gpb1_file(const char *path, int32_t device, pgpb_table **out) {
+  using pgpb::fail;
+  if (!path) return fail(PGPB_EINVAL, "path is NULL");
+  FILE *f = std::fopen(path, "rb");
+  if (!f) return fail(PGPB_EINVAL, std::string("cannot open ") + path);
+  std::vector<unsigned char> buf;
+  unsigned char chunk[1 << 16];
+  size_t n;
+  while ((n = std::fread(chunk, 1, sizeof(chunk), f)) > 0) buf.insert(buf.end(), chunk, chunk + n);
+  std::fclose(f);
+  const int rc = pgpb_table_load_gpb1(buf.data(), int64_t(buf.size()), device, out);
+  if (rc != PGPB_OK) pgpb::set_error(std::string(path) + ": " + pgpb_last_error());
+  return rc;
 }
 
 int pgpb_table_info_get(const pgpb_table *t, pgpb_table_info *out) {

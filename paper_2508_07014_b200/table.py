@@ -57,6 +57,13 @@ class _DeviceTable:
         self._row_max = None
         self._destroy = _lib.LIB.pgpb_table_destroy  # survives interpreter teardown
 
+    @classmethod
+    def _from_handle(cls, handle: int, device: int) -> "_DeviceTable":
+        d = cls.__new__(cls)
+        d.handle, d.device, d._keep, d._row_max = handle, device, None, None
+        d._destroy = _lib.LIB.pgpb_table_destroy
+        return d
+
     def info(self) -> _lib.TableInfo:
         out = _lib.TableInfo()
         _lib.check(_lib.LIB.pgpb_table_info_get(self.handle, _lib.ctypes.byref(out)))
@@ -194,6 +201,46 @@ class ArcTable:
         self.__dict__.update(st)
         self._dev = {}
         self._dev_lock = threading.Lock()
+
+
+class DeviceTable:
+    """A boosting table that lives only on one device: GPB1 bytes parsed,
+    validated and laid out by the native loader (pgpb_table_load_gpb1), with
+    no host ArcTable.  Accepted wherever the API takes a table for device
+    work (get_scores_batch / advance, the greedy and beam decoders)."""
+
+    def __init__(self, dt: _DeviceTable):
+        info = dt.info()
+        self._dt = dt
+        self.num_states = int(info.num_states)
+        self.vocab_size = int(info.vocab_size)
+        self.num_arcs = int(info.num_arcs)
+        self.unk_score = float(info.unk_score)
+        self.device = dt.device
+
+    def device_table(self, device: int | None = None) -> _DeviceTable:
+        if device is not None and int(device) != self.device:
+            raise ValueError(f"table resides on cuda:{self.device}, not cuda:{device}")
+        return self._dt
+
+
+def load_table_device(source, device: int | None = None) -> DeviceTable:
+    """GPB1 file path (or bytes) straight to a device table (table.py:267-310
+    semantics: TableFormatError on a malformed table)."""
+    import torch
+
+    _lib.require_cuda()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    h = _lib.c_void_p()
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        buf = np.frombuffer(bytes(source), dtype=np.uint8)
+        rc = _lib.LIB.pgpb_table_load_gpb1(_lib.ptr(buf) if buf.size else None, buf.size, dev, _lib.ctypes.byref(h))
+    else:
+        rc = _lib.LIB.pgpb_table_load_gpb1_file(str(Path(source)).encode(), dev, _lib.ctypes.byref(h))
+    if rc == _lib.PGPB_EFORMAT:
+        raise TableFormatError(_lib.last_error())
+    _lib.check(rc, "pgpb_table_load_gpb1")
+    return DeviceTable(_DeviceTable._from_handle(h.value, dev))
 
 
 @dataclass(frozen=True)
