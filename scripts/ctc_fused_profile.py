@@ -37,3 +37,5 @@ for name, lp in cr.regimes(B, T, V, torch.device("cuda")).items():
         if lam:
             print("  steps(cyc):", [int(v) for v in buf[16:16 + 60]])
             print("  emit/need :", [int(v) for v in buf[128:128 + 60]])
+            print("  staged", int(buf[248]), "guess done per warp", [int(v) for v in buf[244:248]],
+                  "round0 done per warp", [int(v) for v in buf[240:244]])
