@@ -150,6 +150,20 @@ int pgpb_advance_chain(const pgpb_table *table, const int32_t *d_states, int64_t
                        float *d_scores, int32_t *d_next, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Phrase-hit counting = evaluation.keyphrase_hits / count_occurrences
+ * (evaluation.py:90-134) over a large corpus.  `table` is an Aho-Corasick
+ * table compiled over word ids (phrase words 1..W, any other word 0);
+ * out_start/out_len/out_phrase[state] list the phrases whose end node lies
+ * on the state's failure chain.  n_seqs word sequences, words[offsets[q] ..
+ * offsets[q+1]) for sequence q.  Pass 1 (d_keys == NULL): d_counts[q] =
+ * occurrences in sequence q.  Pass 2: keys phrase * n_seqs + q written from
+ * d_key_offsets[q] (an exclusive scan of the counts).                      */
+int pgpb_phrase_hits(const pgpb_table *table, const int32_t *d_words, const int64_t *d_offsets,
+                     int64_t n_seqs, const int32_t *d_out_start, const int32_t *d_out_len,
+                     const int32_t *d_out_phrase, int32_t *d_counts, int64_t *d_keys,
+                     const int64_t *d_key_offsets, void *stream);
+
+/* ------------------------------------------------------------------------
  * Fused batched greedy CTC = _kernels.ctc_greedy (_kernels.pyx:75-225) /
  * ctc_greedy_boosted (decoding.py:156-229), over B utterances at once.
  * logprobs [B,T,V] f32 C order; lengths[B] (<= T) frames per utterance.
