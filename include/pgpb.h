@@ -221,6 +221,13 @@ typedef struct pgpb_label_loop_state {
   int32_t *states;
   int64_t lmax;
   int32_t cap;       /* max_symbols_per_frame                             */
+  /* TDT (token-and-duration transducer): frames to advance per row, the
+   * argmax of the duration head, or NULL for RNN-T.  A blank advances
+   * max(d, 1) frames; an emission with d > 0 advances d frames and resets
+   * the symbol counter; d == 0 stays on the frame (cap still applies).
+   * No reference counterpart: parity-unpinned extension; with
+   * d = 0 for every emission and d = 1 for blanks it is exactly R7.       */
+  const int32_t *durations;
 } pgpb_label_loop_state;
 
 /* One label-looping iteration fused with its bookkeeping: for every row r

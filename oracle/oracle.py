@@ -370,6 +370,47 @@ def transducer_greedy(step, T, blank, table, lam, max_symbols, enabled=True):
     return {"tokens": toks, "am": am, "boost": boost, "trace": trace}
 
 
+def transducer_greedy_tdt(step, T, blank, table, lam, max_symbols, enabled=True):
+    """TDT greedy (no reference counterpart; the label-looping kernel's rules):
+    step(last_token_or_None, t) -> (f32 row, duration).  Token decisions are
+    R7's (argmax, blank test, boosted rerank excluding blank); a blank adds its
+    log-prob and advances max(d, 1) frames; an emission advances d frames
+    (d > 0) or stays (d == 0) until max_symbols emissions, then advances 1.
+    With d = 1 on blanks and d = 0 on emissions this is transducer_greedy."""
+    use = _active(table, lam, enabled)
+    toks, trace = [], []
+    am = boost = 0.0
+    state, last = 0, None
+    t, k = 0, 0
+    while t < T:
+        row, dur = step(last, t)
+        a = int(np.argmax(row))
+        if a == blank:
+            am += float(row[blank])
+            t += max(int(dur), 1)
+            k = 0
+            continue
+        if use:
+            sc, nx = score_batch(table, [state])
+            ch = _rerank(row, sc[0], lam, (blank,))
+            d, ns = float(sc[0, ch]), int(nx[0, ch])
+        else:
+            ch, d, ns = a, 0.0, 0
+        toks.append(ch)
+        trace.append((ch, d, ns))
+        am += float(row[ch])
+        boost += d
+        state, last = ns, ch
+        k += 1
+        if dur > 0:
+            t += int(dur)
+            k = 0
+        elif k >= max_symbols:
+            t += 1
+            k = 0
+    return {"tokens": toks, "am": am, "boost": boost, "trace": trace}
+
+
 @dataclass
 class _Hyp:
     tokens: tuple

@@ -46,7 +46,8 @@ class LabelLoopState(ctypes.Structure):
     """pgpb_label_loop_state (include/pgpb.h)."""
 
     _fields_ = [(n, c_void_p) for n in ("t", "k", "lengths", "n", "last", "tree", "am", "boost", "tokens",
-                                         "deltas", "states")] + [("lmax", c_int64), ("cap", c_int32)]
+                                         "deltas", "states")] + [("lmax", c_int64), ("cap", c_int32),
+                                                                 ("durations", c_void_p)]
 
 
 class BeamHyps(ctypes.Structure):

@@ -121,8 +121,9 @@ __global__ void __launch_bounds__(kThreads)
       // R7 bookkeeping (decoding.py:371-392)
       st.am[r] = st.am[r] + static_cast<double>(d.lp);
       int64_t tn = tr;
+      const int dur = st.durations ? st.durations[r] : -1;  // TDT duration head argmax, or RNN-T
       if (d.blank) {
-        tn = tr + 1;
+        tn = tr + (dur > 1 ? dur : 1);
         st.k[r] = 0;
         emit[r] = 0;
         feed[r] = st.last[r];
@@ -137,7 +138,10 @@ __global__ void __launch_bounds__(kThreads)
         st.boost[r] = st.boost[r] + d.delta;
         st.tree[r] = d.next;
         const int64_t k = st.k[r] + 1;
-        if (k >= st.cap) {  // symbol cap: next frame, no blank score
+        if (dur > 0) {  // TDT: the emission also consumes dur frames
+          tn = tr + dur;
+          st.k[r] = 0;
+        } else if (k >= st.cap) {  // symbol cap: next frame, no blank score
           tn = tr + 1;
           st.k[r] = 0;
         } else {

@@ -17,6 +17,14 @@ iteration is a fixed sequence of kernels (joint GEMMs, log-softmax, the
 fused step, the LSTM cell), captured once as a CUDA graph and replayed; the
 host only polls an "all done" flag every `poll` iterations.
 
+TDT (token-and-duration transducer, NeMo's label-looping greedy): a model
+built with a duration set adds a duration head; each iteration also passes
+every row's duration argmax to the fused step, which advances blanks by
+max(d, 1) frames and emissions by d frames (d == 0: stay, cap applies).  The
+reference has no TDT, so this is a parity-unpinned extension,
+checked against its own restatement (oracle.transducer_greedy_tdt), which
+reduces to R7 when every emission has d = 0 and every blank d = 1.
+
 The networks are random-init stand-ins of the paper's shapes (1-layer
 LSTM-640 prediction net + joint) — library GEMMs, outside
 the GPU-PB path.  Parity with the reference decoder is established by
@@ -51,8 +59,12 @@ class RNNTModel:
     """
 
     def __init__(self, vocab_size: int, enc_dim: int = 512, pred_dim: int = 640, joint_dim: int = 640,
-                 blank_id: int = 0, seed: int = 0, device="cuda", dtype=None, blank_bias: float = 3.0):
-        """dtype defaults to bfloat16 (tensor-core GEMMs); log-probs are float32."""
+                 blank_id: int = 0, seed: int = 0, device="cuda", dtype=None, blank_bias: float = 3.0,
+                 durations: tuple[int, ...] | None = None):
+        """dtype defaults to bfloat16 (tensor-core GEMMs); log-probs are float32.
+
+        durations: TDT duration set (e.g. (0, 1, 2, 3, 4)); adds a duration
+        head to the joint (NeMo's token-and-duration transducer)."""
         torch = _torch()
         g = torch.Generator(device="cpu")
         g.manual_seed(seed)
@@ -75,6 +87,12 @@ class RNNTModel:
         self.w_out = w(V, J, fan_in=J) * 3.0  # peaky enough for confident argmaxes
         self.b_out = torch.zeros(V, device=device, dtype=dt)
         self.b_out[blank_id] = blank_bias  # blank-dominated frames, as trained transducers are
+        self.durations = tuple(int(d) for d in durations) if durations else None
+        if self.durations:
+            if min(self.durations) < 0:
+                raise ValueError("durations must be >= 0")
+            self.w_dur = w(len(self.durations), J, fan_in=J) * 3.0
+            self.dur_values = torch.tensor(self.durations, device=device, dtype=torch.int32)
 
     def project_encoder(self, enc):
         """enc [B,T,D] -> [B,T,J] (computed once per batch)."""
@@ -88,10 +106,19 @@ class RNNTModel:
 
     def joint_logprobs(self, enc_proj_t, pred_h):
         """[B,J] encoder projection at each row's frame + [B,H] -> [B,V] float32 log-probs."""
+        return self.joint(enc_proj_t, pred_h)[0]
+
+    def joint(self, enc_proj_t, pred_h):
+        """Token log-probs [B,V] f32 and, for TDT, each row's duration (argmax of
+        the duration head, first max) as int32 frames; None for RNN-T."""
         torch = _torch()
         z = torch.relu(enc_proj_t + torch.addmm(self.b_joint, pred_h, self.w_pred.T))
         logits = torch.addmm(self.b_out, z, self.w_out.T)
-        return torch.log_softmax(logits.float(), dim=-1)
+        lp = torch.log_softmax(logits.float(), dim=-1)
+        if not self.durations:
+            return lp, None
+        dl = (z @ self.w_dur.T).float()
+        return lp, self.dur_values[torch.argmax(dl, dim=-1)]
 
 
 @dataclass
@@ -149,6 +176,7 @@ class LabelLoopingDecoder:
         self.emit = torch.zeros(B, device=d, dtype=torch.uint8)
         self.feed = torch.zeros(B, device=d, dtype=i64)
         self.lp = torch.zeros((B, model.V), device=d, dtype=f32)
+        self.dur = torch.zeros(B, device=d, dtype=i32) if model.durations else None
         self.any_active = torch.zeros(1, device=d, dtype=i32)
         self.flag_host = torch.zeros(1, dtype=i32, pin_memory=True)
         self.rows = torch.arange(B, device=d)
@@ -156,14 +184,17 @@ class LabelLoopingDecoder:
         p = lambda x: x.data_ptr()  # noqa: E731
         self.state = _lib.LabelLoopState(p(self.t), p(self.k), p(self.lengths), p(self.n), p(self.last), p(self.tree),
                                          p(self.am), p(self.boost), p(self.tokens), p(self.deltas), p(self.states),
-                                         self.Lmax, self.cap)
+                                         self.Lmax, self.cap, p(self.dur) if self.dur is not None else None)
 
     # -- one label iteration (fixed kernel sequence) ------------------------
     def _iteration(self):
         torch, m = self.torch, self.model
         self.any_active.zero_()
         tf = torch.minimum(self.t, (self.lengths - 1).clamp(min=0))
-        self.lp.copy_(m.joint_logprobs(self.enc_proj[self.rows, tf], self.h))
+        lp, dur = m.joint(self.enc_proj[self.rows, tf], self.h)
+        self.lp.copy_(lp)
+        if dur is not None:
+            self.dur.copy_(dur)
         _lib.check(_lib.LIB.pgpb_label_loop_step(
             self.handle, self.lp.data_ptr(), self.V, self.B, self.V, int(m.blank_id), float(self.cfg.lam),
             int(self.use), _lib.ctypes.byref(self.state), self.emit.data_ptr(), self.feed.data_ptr(),
@@ -220,7 +251,10 @@ class LabelLoopingDecoder:
                     t0, last0 = self.t.clone(), self.last.clone()
                     active = (t0 < self.lengths).cpu().numpy()
                     self._iteration()
-                    records.append((self.lp.cpu().numpy().copy(), active, t0.cpu().numpy(), last0.cpu().numpy()))
+                    rec = (self.lp.cpu().numpy().copy(), active, t0.cpu().numpy(), last0.cpu().numpy())
+                    if self.dur is not None:
+                        rec = rec + (self.dur.cpu().numpy().copy(),)
+                    records.append(rec)
                 elif self.graph is not None:
                     self.graph.replay()
                 else:

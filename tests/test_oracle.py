@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import gen_inputs as gi
-from conftest import golden, golden_npz, golden_tree_case
+from conftest import golden, golden_npz, golden_tree_case, product_table
 
 from oracle import oracle as orc
 
@@ -169,3 +169,21 @@ def test_oracle_matches_reference_cython_kernels():
             y = ref.ctc_greedy(lp, 0, lam, lam != 0, *orc._tab_arrays(t))
             assert np.array_equal(x[0], y[0]) and x[1] == y[1] and x[2] == y[2]
             assert np.array_equal(x[3], y[3]) and np.array_equal(x[4], y[4])
+
+
+def test_tdt_restatement_reduces_to_r7():
+    """CPU-side sanity of the restatement: d = 0 on emissions, 1 on blanks == R7."""
+    rng = np.random.default_rng(3)
+    phrases, V, c0, beta = gi.random_tree_spec(rng, max_phrases=10, max_len=4, max_vocab=12)
+    tab = product_table(phrases, V, c0, beta)
+    rows, default = gi.random_transducer_rows(rng, V)
+
+    def step(last, t):
+        return rows.get("" if last is None else str(int(last)), default)
+
+    def step_tdt(last, t):
+        r = step(last, t)
+        return r, (1 if int(np.argmax(r)) == 0 else 0)
+
+    for lam in (0.0, 1.0):
+        assert orc.transducer_greedy_tdt(step_tdt, 7, 0, tab, lam, 3) == orc.transducer_greedy(step, 7, 0, tab, lam, 3)
