@@ -275,7 +275,10 @@ struct Smem {
   int32_t *fa, *ft2, *in_off, *in_last, *o_tok, *o_nx;
   float *flpa, *flp2, *o_s, *o_lp;
   int32_t *c_soff, *c_slast, *c_eoff, *c_elast, *c_act, *c_sst, *c_est;  // [C]
-  int32_t *misc;  // [0] seg start off, [1] seg start last, [2] emitted so far, [3] seg start state
+  int32_t *misc;  // [0] seg start off, [1] seg start last, [2] emitted so far, [3] seg start state,
+                  // [4] first frame whose walked log-prob differs from its argmax's
+  double *ck;     // am before frames 0, 32, 64, ... of the segment (accountant warp)
+  double *dsum;   // [0] am, [1] boost: running totals across segments
   int32_t *wsum;  // [33] scan scratch
 };
 
@@ -284,7 +287,8 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 __host__ __device__ inline size_t smem_bytes(int Vp, int Vw, int W, int TS, int use_boost, Smem *s,
                                              unsigned char *base) {
   const int C = 32 * W;
-  const size_t vb = use_boost ? size_t(Vp) * 4 : 0, fb = align16(size_t(TS) * 4), cb = align16(size_t(C) * 4);
+  const size_t vb = use_boost ? size_t(Vp) * 4 : 0, fb = align16(size_t(TS) * 4),
+               cb = align16(size_t(C + 32) * 4);  // + the accountant warp's (never live) lanes
   size_t o = 0;
 #define PGPB_TAKE(field, type, bytes)                     \
   do {                                                    \
@@ -313,6 +317,8 @@ __host__ __device__ inline size_t smem_bytes(int Vp, int Vw, int W, int TS, int 
   PGPB_TAKE(c_sst, int32_t, cb);
   PGPB_TAKE(c_est, int32_t, cb);
   PGPB_TAKE(misc, int32_t, 8 * 4);
+  PGPB_TAKE(ck, double, (size_t(TS) / 32 + 2) * 8);
+  PGPB_TAKE(dsum, double, 2 * 8);
   PGPB_TAKE(wsum, int32_t, 33 * 4);
 #undef PGPB_TAKE
   return o;
@@ -740,11 +746,11 @@ __device__ void seq_walk(const Ctx &x, unsigned *bm, int n, int &off, int &st, i
 // Named barrier + OR over the CTA (all warps walk).
 __device__ __forceinline__ bool cta_or(bool pred) { return __syncthreads_or(pred) != 0; }
 
-__global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g) {
+__global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(Args g) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const TableView &t = g.t;
   const int V = g.V, Vp = (V + 3) & ~3, Vw = (V + 31) >> 5;
-  const int W = blockDim.x >> 5, C = 32 * W, TS = g.TS;
+  const int W = (blockDim.x >> 5) - 1, C = 32 * W, TS = g.TS;  // walker warps + 1 accountant warp
   const bool boost = g.use_boost != 0;
   Smem s;
   smem_bytes(Vp, Vw, W, TS, g.use_boost, &s, smem_raw);
@@ -775,13 +781,15 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
 
   for (int64_t b = blockIdx.x; b < g.B; b += gridDim.x) {
     const int64_t Tb = g.lengths ? int64_t(__ldg(g.lengths + b)) : g.T;
-    double am = 0.0, bo = 0.0;  // warp 0: am (and boost when W == 1); warp 1: boost
+    double am = 0.0;  // accountant lane 0
     __syncthreads();
     if (threadIdx.x == 0) {
       s.misc[0] = root_off;
       s.misc[1] = -1;
       s.misc[2] = 0;
       s.misc[3] = 0;
+      s.dsum[0] = 0.0;
+      s.dsum[1] = 0.0;
     }
 #ifdef PGPB_SEQ_PROFILE
     const long long t_start = clock64();
@@ -803,6 +811,35 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
         }
       }
       __syncthreads();
+      // Accountant warp: am = sum of the argmax log-probs in frame order (the
+      // reference's fp64 rounding sequence), with a checkpoint every 32
+      // frames, while the walkers decide.  Exact when unboosted; when
+      // boosted it is the final am unless a walked decision picked a token
+      // other than its frame's argmax (checked and repaired in the tail).
+      if (wid == W && lane == 0) {
+#ifdef PGPB_SEQ_PROFILE
+        const long long t0 = clock64();
+#endif
+        double acc = s.dsum[0];
+        for (int f0 = 0; f0 < n; f0 += 32) {
+          s.ck[f0 >> 5] = acc;
+          const int e = min(f0 + 32, n);
+          int f = f0;
+          for (; f + 8 <= e; f += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = s.flpa[f + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, static_cast<double>(v[u]));
+          }
+          for (; f < e; ++f) acc = __dadd_rn(acc, static_cast<double>(s.flpa[f]));
+        }
+        am = acc;
+#ifdef PGPB_SEQ_PROFILE
+        if (blockIdx.x == 0) CF_COUNT(13, clock64() - t0);
+#endif
+      }
+      if (threadIdx.x == 0) s.misc[4] = n;
       bool seq = false;
       if (boost) {
         // Boost-sensitive frames: may emit and the top-2 gap is within the
@@ -987,39 +1024,26 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
         }
       }
       __syncthreads();
-      // ---- tail: ordered sums, compaction ----
-      // am (warp 0) and boost (warp 1, or warp 0 when alone) are two
-      // independent fp64 chains in frame order, the reference's rounding
-      // sequence; each warp loads 32 frames at a time and walks them by
-      // shuffle (+ 0.0 for a frame without an emission is exact).
-      if ((wid == 0 || (wid == 1 && boost)) && lane == 0) {
-#ifdef PGPB_SEQ_PROFILE
-        const long long t0 = clock64();
-#endif
-        const bool do_am = wid == 0, do_bo = boost && (wid == 1 || W == 1);
-        int f = 0;
-        for (; f + 8 <= n; f += 8) {
-          float l8[8], s8[8];
-          int t8[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            l8[u] = s.o_lp[f + u];
-            t8[u] = s.o_tok[f + u];
-            s8[u] = boost ? s.o_s[f + u] : 0.0f;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (do_am) am = __dadd_rn(am, static_cast<double>(l8[u]));
-            if (do_bo) bo = __dadd_rn(bo, t8[u] >= 0 ? static_cast<double>(s8[u]) : 0.0);
-          }
+      // ---- tail: repair am if needed, boost sum, compaction ----
+      if (boost) {
+        for (int f = threadIdx.x; f < n; f += nthreads)
+          if (__float_as_int(s.o_lp[f]) != __float_as_int(s.flpa[f])) atomicMin(s.misc + 4, f);
+      }
+      __syncthreads();
+      if (wid == W && lane == 0) {
+        const int fs = s.misc[4];
+        if (fs < n) {  // a walked decision left the argmax path: re-add from the checkpoint
+          double acc = s.ck[fs >> 5];
+          for (int f = fs & ~31; f < n; ++f) acc = __dadd_rn(acc, static_cast<double>(s.o_lp[f]));
+          am = acc;
         }
-        for (; f < n; ++f) {
-          if (do_am) am = __dadd_rn(am, static_cast<double>(s.o_lp[f]));
-          if (do_bo) bo = __dadd_rn(bo, s.o_tok[f] >= 0 ? static_cast<double>(s.o_s[f]) : 0.0);
-        }
-#ifdef PGPB_SEQ_PROFILE
-        if (blockIdx.x == 0 && threadIdx.x == 0) CF_COUNT(13, clock64() - t0);
-#endif
+        s.dsum[0] = am;
+      }
+      if (boost && threadIdx.x == 0) {  // boost: emitted frames only (+ 0.0 elsewhere is the identity)
+        double acc = s.dsum[1];
+        for (int f = 0; f < n; ++f)
+          if (s.o_tok[f] >= 0) acc = __dadd_rn(acc, static_cast<double>(s.o_s[f]));
+        s.dsum[1] = acc;
       }
       // block exclusive scan of emit flags over n frames
       const int q = (n + nthreads - 1) / nthreads;
@@ -1036,7 +1060,7 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
       __syncthreads();
       if (threadIdx.x == 0) {
         int acc = 0;
-        for (int w = 0; w < W; ++w) {
+        for (int w = 0; w <= W; ++w) {
           const int v = s.wsum[w];
           s.wsum[w] = acc;
           acc += v;
@@ -1075,10 +1099,9 @@ __global__ void __launch_bounds__(32 * kMaxConsumers, 1) ctc_walk_kernel(Args g)
 #endif
     if (threadIdx.x == 0) {
       g.nout[b] = s.misc[2];
-      g.am_out[b] = am;
-      if (!boost || W == 1) g.boost_out[b] = bo;
+      g.am_out[b] = s.dsum[0];
+      g.boost_out[b] = s.dsum[1];
     }
-    if (threadIdx.x == 32 && boost) g.boost_out[b] = bo;
   }
 }
 
@@ -1152,12 +1175,12 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
     }
   }
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctc_walk_kernel, 32 * W, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctc_walk_kernel, 32 * (W + 1), smem);
   const int64_t cap = int64_t(sm_count(current_device())) * std::max(per_sm, 1);
   const unsigned grid = unsigned(B < cap ? B : cap);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(32 * W);
+  cfg.blockDim = dim3(32 * (W + 1));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
