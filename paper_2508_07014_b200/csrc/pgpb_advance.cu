@@ -627,8 +627,27 @@ static int launch_advance(const pgpb_table *table, const int32_t *d_states, int6
   if (variant == 6 && vec && smem_root) {
     const int Vw = (t.vocab_size + 31) >> 5;
     const size_t wbytes = (size_t(Vw) * 8 + 15) & ~size_t(15);
+    // Geometry: 4 CTAs per SM (64 registers per thread); rows go to warps
+    // round-robin inside a CTA, so pick the warp count (4..8) that divides
+    // the CTA's rows most evenly (8192 rows: 14 per CTA on 7 warps, measured
+    // best of the 3..6 x 4..8 grid).
     const char *e = getenv("PGPB_V6_CTAS");
+    const char *ew = getenv("PGPB_V6_WARPS");
     const int per_sm = e ? std::max(1, atoi(e)) : 4;
+    int W = kWarpsPerBlock;
+    {
+      const int64_t c = int64_t(nsm) * per_sm;
+      const int64_t r = std::max<int64_t>(1, (B + c - 1) / c);
+      double best = 1e30;
+      for (int w = kWarpsPerBlock; w >= 4; --w) {
+        const double cost = double((r + w - 1) / w) / (double(r) / double(w));
+        if (cost < best - 1e-9) {
+          best = cost;
+          W = w;
+        }
+      }
+      if (ew) W = std::max(1, std::min(kWarpsPerBlock, atoi(ew)));
+    }
     int64_t ctas = int64_t(nsm) * per_sm;
     int rows = int((B + ctas - 1) / ctas);
     if (rows < 1) rows = 1;
@@ -641,7 +660,7 @@ static int launch_advance(const pgpb_table *table, const int32_t *d_states, int6
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem6)));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(unsigned(ctas));
-      cfg.blockDim = dim3(kThreads);
+      cfg.blockDim = dim3(32 * W);
       cfg.dynamicSmemBytes = smem6;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];

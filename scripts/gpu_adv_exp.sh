@@ -1,6 +1,6 @@
 cd $GRAFT_REPO_ROOT
 timeout 600 python -m pytest tests/test_advance_gpu.py -x -q > gpurun_out/adv_tests.log 2>&1; echo rc=$? >> gpurun_out/adv_tests.log
-for env in "X=0" "PGPB_V6_CTAS=3" "PGPB_V6_CTAS=5" "PGPB_V6_CTAS=8" "PGPB_V6_DEBUG_SKIP=1"; do
+for env in "X=0" "X=1" "PGPB_V6_WARPS=8"; do
   echo "$env" >> gpurun_out/adv_exp.log
   env $env timeout 300 python bench.py --no-decode --no-cpu-baseline 2>&1 | python -c "import json,sys; d=json.loads([l for l in sys.stdin if l.startswith('{')][0]); print(d['ms_per_step'], d['roofline']['frac'])" >> gpurun_out/adv_exp.log
 done
