@@ -373,8 +373,36 @@ __device__ __forceinline__ bool may_win(const Ctx &x, const BCand &best, float s
 // Registers hold the tokens and scores of up to kLaneArcs arcs (one load
 // batch); candidates carry the arc index (or -1 for a dense token) and only
 // the winner's successor is resolved.
+#ifdef PGPB_SEQ_PROFILE
+__device__ int g_ld_n;
+__device__ long long g_ld_rec[256][4];
+#endif
+__device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row, int off, int st, int last, int a,
+                                                 float lpa, int t2, float lp2, BCand &out, int &path);
 __device__ __forceinline__ bool lane_decide(const Ctx &x, const float *row, int off, int st, int last, int a,
                                             float lpa, int t2, float lp2, BCand &out) {
+#ifdef PGPB_SEQ_PROFILE
+  const long long t0 = clock64();
+  int path = 0;
+  const bool r = lane_decide_impl(x, row, off, st, last, a, lpa, t2, lp2, out, path);
+  const long long dt = clock64() - t0;
+  if (blockIdx.x == 0) {
+    const int i = atomicAdd(&g_ld_n, 1);
+    if (i < 256) {
+      g_ld_rec[i][0] = dt;
+      g_ld_rec[i][1] = __ldg(&x.t->blob[off].x);
+      g_ld_rec[i][2] = path * 10 + (r ? 1 : 0);
+      g_ld_rec[i][3] = threadIdx.x;
+    }
+  }
+  return r;
+#else
+  int path = 0;
+  return lane_decide_impl(x, row, off, st, last, a, lpa, t2, lp2, out, path);
+#endif
+}
+__device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row, int off, int st, int last, int a,
+                                                 float lpa, int t2, float lp2, BCand &out, int &path) {
   const int4 *blob = x.t->blob + off;
   const int4 h = __ldg(blob);
   const float *root = x.s->root;
@@ -385,7 +413,66 @@ __device__ __forceinline__ bool lane_decide(const Ctx &x, const float *row, int 
     const uint32_t wa = __ldg(wb + (a >> 5));
     const uint32_t wt = t2 < x.V ? __ldg(wb + (t2 >> 5)) : 0u;
     const bool a_in = (wa >> (a & 31)) & 1u, t2_in = t2 < x.V && ((wt >> (t2 & 31)) & 1u);
-    if (!a_in && !t2_in) {
+    if (a_in || t2_in) {
+      // Semi-fast path: a and/or t2 are closure tokens.  Their arcs are
+      // found by binary search over the token-sorted arcs (a few L1 hits);
+      // every other arc ranks after t2 and scores at most smax (header), so
+      // when smax clears the crossing point of the bound the {a, t2}
+      // candidates decide exactly, without scanning the closure.
+      const int count = h.x;
+      const float acc = __int_as_float(h.y), smax = __int_as_float(h.w);
+      auto find = [&](int v, int4 &hit) {
+        int lo = 0, hi = count - 1;
+        while (lo <= hi) {
+          const int mid = (lo + hi) >> 1;
+          const int4 e = __ldg(blob + 1 + mid);
+          if (e.x == v) {
+            hit = e;
+            return true;
+          }
+          if (e.x < v)
+            lo = mid + 1;
+          else
+            hi = mid - 1;
+        }
+        return false;
+      };
+      int4 ea = make_int4(0, 0, 0, 0), et = make_int4(0, 0, 0, 0);
+      if (a_in) find(a, ea);
+      if (t2_in) find(t2, et);
+      BCand best = bcand_none();
+      int fid;
+      float flp;
+      if (a_in) {
+        const float sv = __int_as_float(ea.z);
+        bcand_consider(best, fuse(lpa, x.lam, sv), lpa, a, sv, ea.y, ea.w);
+        fid = t2;
+        flp = lp2;
+      } else {
+        const float sv = acc + root[a];
+        bcand_consider(best, fuse(lpa, x.lam, sv), lpa, a, sv, x.s->rnext[a], x.s->rnoff[a]);
+        const bool amax = root[a] == x.max_root;
+        fid = amax ? a : t2;
+        flp = amax ? lpa : lp2;
+      }
+      if (t2 < x.V && t2 != x.blank && t2 != last) {
+        if (t2_in) {
+          const float sv = __int_as_float(et.z);
+          bcand_consider(best, fuse(lp2, x.lam, sv), lp2, t2, sv, et.y, et.w);
+        } else if (fid == t2) {
+          const float sv = acc + root[t2];
+          bcand_consider(best, fuse(lp2, x.lam, sv), lp2, t2, sv, x.s->rnext[t2], x.s->rnoff[t2]);
+        }
+      }
+      if (x.lam > 0.0 && isfinite(best.c) && isfinite(lp2)) {
+        const double sx = (best.c - static_cast<double>(lp2)) / x.lam;
+        const float s_lo = static_cast<float>(sx - (fabs(sx) * 1e-6 + 1e-6));
+        if (smax < s_lo && certified(x, best, acc, fid, flp)) {
+          out = best;
+          return true;
+        }
+      }
+    } else {
       const float acc = __int_as_float(h.y), smax = __int_as_float(h.w);
       BCand best = bcand_none();
       const float sa = acc + root[a];
@@ -400,7 +487,9 @@ __device__ __forceinline__ bool lane_decide(const Ctx &x, const float *row, int 
       if (x.lam > 0.0 && isfinite(best.c) && isfinite(lp2)) {
         const double sx = (best.c - static_cast<double>(lp2)) / x.lam;
         const float s_lo = static_cast<float>(sx - (fabs(sx) * 1e-6 + 1e-6));
+        path = 1;
         if (smax < s_lo && certified(x, best, acc, fid, flp)) {
+          path = 2;
           out = best;
           out.nx = x.s->rnext[best.v];
           out.noff = x.s->rnoff[best.v];
@@ -1199,6 +1288,15 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
 }  // namespace pgpb
 
 #ifdef PGPB_SEQ_PROFILE
+extern "C" int pgpb_debug_ctc_lane_records(long long *h_out, int reset) {
+  cudaMemcpyFromSymbol(h_out, pgpb::cw::g_ld_rec, sizeof(long long) * 256 * 4);
+  if (reset) {
+    int z = 0;
+    cudaMemcpyToSymbol(pgpb::cw::g_ld_n, &z, sizeof(int));
+  }
+  return 0;
+}
+
 extern "C" int pgpb_debug_ctc_fused_profile(unsigned long long *h_out, int reset) {
   cudaMemcpyFromSymbol(h_out, pgpb::cw::g_cf_prof, sizeof(unsigned long long) * 256);
   if (reset) {

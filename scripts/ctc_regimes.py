@@ -20,7 +20,7 @@ from paper_2508_07014_b200.context import Vocabulary  # noqa: E402
 
 
 def table():
-    phrases, V = gi.corpus("p20k_v1024")
+    phrases, V = gi.corpus(os.environ.get("PGPB_BENCH_CORPUS", "p20k_v1024"))
     ctx = pb.ContextList([pb.Phrase(" ".join(map(str, p)), p) for p in phrases], min_chars=0)
     return pb.compile_arc_table(pb.compute_fail_links(pb.build_prefix_tree(ctx, pb.TreeParams(), V))), V
 
