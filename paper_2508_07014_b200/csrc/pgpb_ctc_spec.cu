@@ -900,34 +900,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         }
       }
       __syncthreads();
-      // Accountant warp: am = sum of the argmax log-probs in frame order (the
-      // reference's fp64 rounding sequence), with a checkpoint every 32
-      // frames, while the walkers decide.  Exact when unboosted; when
-      // boosted it is the final am unless a walked decision picked a token
-      // other than its frame's argmax (checked and repaired in the tail).
-      if (wid == W && lane == 0) {
-#ifdef PGPB_SEQ_PROFILE
-        const long long t0 = clock64();
-#endif
-        double acc = s.dsum[0];
-        for (int f0 = 0; f0 < n; f0 += 32) {
-          s.ck[f0 >> 5] = acc;
-          const int e = min(f0 + 32, n);
-          int f = f0;
-          for (; f + 8 <= e; f += 8) {
-            float v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = s.flpa[f + u];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, static_cast<double>(v[u]));
-          }
-          for (; f < e; ++f) acc = __dadd_rn(acc, static_cast<double>(s.flpa[f]));
-        }
-        am = acc;
-#ifdef PGPB_SEQ_PROFILE
-        if (blockIdx.x == 0) CF_COUNT(13, clock64() - t0);
-#endif
-      }
       if (threadIdx.x == 0) s.misc[4] = n;
       bool seq = false;
       if (boost) {
@@ -955,6 +927,34 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         }
         seq = g.seq_mode == 1 || (g.seq_mode == 0 && 4 * ts > tc && tc >= 8);
         __syncthreads();
+      }
+      // Accountant warp: am = sum of the argmax log-probs in frame order (the
+      // reference's fp64 rounding sequence), with a checkpoint every 32
+      // frames, while the walkers decide.  Exact when unboosted; when
+      // boosted it is the final am unless a walked decision picked a token
+      // other than its frame's argmax (checked and repaired in the tail).
+      if (wid == W && lane == 0) {
+#ifdef PGPB_SEQ_PROFILE
+        const long long t0 = clock64();
+#endif
+        double acc = s.dsum[0];
+        for (int f0 = 0; f0 < n; f0 += 32) {
+          s.ck[f0 >> 5] = acc;
+          const int e = min(f0 + 32, n);
+          int f = f0;
+          for (; f + 8 <= e; f += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = s.flpa[f + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, static_cast<double>(v[u]));
+          }
+          for (; f < e; ++f) acc = __dadd_rn(acc, static_cast<double>(s.flpa[f]));
+        }
+        am = acc;
+#ifdef PGPB_SEQ_PROFILE
+        if (blockIdx.x == 0) CF_COUNT(13, clock64() - t0);
+#endif
       }
       if (boost && seq) {
         // ---- sequential mode: warp 0 walks the segment ----
@@ -1128,11 +1128,52 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         }
         s.dsum[0] = am;
       }
-      if (boost && threadIdx.x == 0) {  // boost: emitted frames only (+ 0.0 elsewhere is the identity)
-        double acc = s.dsum[1];
-        for (int f = 0; f < n; ++f)
-          if (s.o_tok[f] >= 0) acc = __dadd_rn(acc, static_cast<double>(s.o_s[f]));
-        s.dsum[1] = acc;
+      if (boost && wid == 0) {
+        // boost += the emitted frames' deltas in frame order (+ 0.0 for the
+        // others is the identity).  When every value (and the carry) is a
+        // multiple of 2^e and the sum of their magnitudes is below 2^(53+e),
+        // every partial sum in any order is exact in fp64, so the warp may
+        // add them as a tree and match the sequential sum bit for bit; the
+        // deltas are f32 scores of modest size, so this is the normal case.
+        // Otherwise one lane adds them sequentially.
+        const double carry = s.dsum[1];
+        double part = 0.0, sabs = 0.0;
+        int emin = INT_MAX;
+        for (int f = lane; f < n; f += 32) {
+          if (s.o_tok[f] < 0) continue;
+          const float d = s.o_s[f];
+          if (d == 0.0f) continue;
+          int e;
+          frexpf(d, &e);
+          emin = min(emin, max(e - 24, -149));
+          part = __dadd_rn(part, static_cast<double>(d));
+          sabs = __dadd_rn(sabs, fabs(static_cast<double>(d)));
+        }
+        if (carry != 0.0) {
+          int e;
+          frexp(carry, &e);
+          if (lane == 0) {
+            emin = min(emin, e - 53);
+            sabs = __dadd_rn(sabs, fabs(carry));
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          part = __dadd_rn(part, __shfl_xor_sync(kFull, part, o));
+          sabs = __dadd_rn(sabs, __shfl_xor_sync(kFull, sabs, o));
+          emin = min(emin, __shfl_xor_sync(kFull, emin, o));
+        }
+        const bool exact = emin == INT_MAX || (emin > -1000 && sabs * (1.0 + 1e-12) < ldexp(1.0, 53 + emin));
+        if (lane == 0) {
+          if (exact) {
+            s.dsum[1] = __dadd_rn(carry, part);
+          } else {
+            double acc = carry;
+            for (int f = 0; f < n; ++f)
+              if (s.o_tok[f] >= 0) acc = __dadd_rn(acc, static_cast<double>(s.o_s[f]));
+            s.dsum[1] = acc;
+          }
+        }
       }
       // block exclusive scan of emit flags over n frames
       const int q = (n + nthreads - 1) / nthreads;

@@ -194,3 +194,17 @@ def test_empty_and_single_frame_batches(t20k):
     lps = np.stack([gi.random_emissions(rng, 5, V) for _ in range(7)])
     lens = np.array([0, 1, 0, 5, 2, 0, 1], dtype=np.int32)
     _check(_run(lps, lens, tab, 1.0), lps, lens, tab, 1.0)
+
+
+def test_boost_sum_fallback_wide_dynamic_range(t20k):
+    """Depth-1 arcs of 1e-7 and deeper arcs of ~1e6: the boost
+    deltas span more than 53 bits, so the walker's exact tree sum must fall
+    back to the sequential fp64 sum (still bit-exact)."""
+    phrases, V, _ = t20k
+    tab = product_table(phrases, V, c0=1e-7, beta=1e13)  # depth-1 arcs 1e-7, deeper arcs ~1e6
+    rng = np.random.default_rng(38)
+    B, T = 12, 300
+    lps = np.stack([_phrase_emissions(rng, phrases, T, V) for _ in range(B)])
+    got = _run(lps, None, tab, 1.0)
+    _check(got, lps, None, tab, 1.0)
+    assert any(abs(r.boost_score) > 1e5 for r in got)
