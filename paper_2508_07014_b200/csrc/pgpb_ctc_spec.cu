@@ -832,6 +832,42 @@ __device__ void seq_walk(const Ctx &x, unsigned *bm, int n, int &off, int &st, i
   __syncwarp();
 }
 
+// Exact warp sum of f32 values added to a fp64 carry.  When every value
+// (and the carry) is a multiple of 2^e and the sum of their magnitudes is
+// below 2^(53+e), every partial sum in any order is representable in fp64,
+// so a tree sum equals the reference's sequential sum bit for bit; returns
+// false (and no sum) otherwise.  Call with all 32 lanes; lane l passes the
+// values it owns through `next(i)` for i = 0, 1, ... until it returns false.
+template <typename Next>
+__device__ __forceinline__ bool exact_warp_sum(double carry, Next next, double &out) {
+  double part = 0.0, sabs = 0.0;
+  int emin = INT_MAX;
+  float d;
+  while (next(d)) {
+    if (d == 0.0f) continue;
+    int e;
+    frexpf(d, &e);
+    emin = min(emin, max(e - 24, -149));
+    part = __dadd_rn(part, static_cast<double>(d));
+    sabs = __dadd_rn(sabs, fabs(static_cast<double>(d)));
+  }
+  if (carry != 0.0 && (threadIdx.x & 31) == 0) {
+    int e;
+    frexp(carry, &e);
+    emin = min(emin, e - 53);
+    sabs = __dadd_rn(sabs, fabs(carry));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    part = __dadd_rn(part, __shfl_xor_sync(kFull, part, o));
+    sabs = __dadd_rn(sabs, __shfl_xor_sync(kFull, sabs, o));
+    emin = min(emin, __shfl_xor_sync(kFull, emin, o));
+  }
+  const bool exact = emin == INT_MAX || (emin > -1000 && sabs * (1.0 + 1e-12) < ldexp(1.0, 53 + emin));
+  out = __dadd_rn(carry, part);
+  return exact;
+}
+
 // Named barrier + OR over the CTA (all warps walk).
 __device__ __forceinline__ bool cta_or(bool pred) { return __syncthreads_or(pred) != 0; }
 
@@ -933,7 +969,7 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
       // frames, while the walkers decide.  Exact when unboosted; when
       // boosted it is the final am unless a walked decision picked a token
       // other than its frame's argmax (checked and repaired in the tail).
-      if (wid == W && lane == 0) {
+      if (boost && wid == W && lane == 0) {  // (unboosted: the tail's exact tree sum, see below)
 #ifdef PGPB_SEQ_PROFILE
         const long long t0 = clock64();
 #endif
@@ -1119,58 +1155,57 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
           if (__float_as_int(s.o_lp[f]) != __float_as_int(s.flpa[f])) atomicMin(s.misc + 4, f);
       }
       __syncthreads();
-      if (wid == W && lane == 0) {
-        const int fs = s.misc[4];
-        if (fs < n) {  // a walked decision left the argmax path: re-add from the checkpoint
-          double acc = s.ck[fs >> 5];
-          for (int f = fs & ~31; f < n; ++f) acc = __dadd_rn(acc, static_cast<double>(s.o_lp[f]));
-          am = acc;
+      if (wid == W) {
+        // am over every frame in order: the exact warp tree sum when it is
+        // exact (the usual case), else the accountant's sequential sum
+        // (boosted: computed during the walk and repaired from the first
+        // off-argmax frame; unboosted: computed here)
+        int f = lane;
+        double tree;
+        const bool exact = exact_warp_sum(s.dsum[0], [&](float &v) {
+          if (f >= n) return false;
+          v = s.o_lp[f];
+          f += 32;
+          return true;
+        }, tree);
+        if (lane == 0) {
+          if (exact) {
+            am = tree;
+          } else if (!boost) {
+            double acc = s.dsum[0];
+            for (int u = 0; u < n; ++u) acc = __dadd_rn(acc, static_cast<double>(s.o_lp[u]));
+            am = acc;
+          } else {
+            const int fs = s.misc[4];
+            if (fs < n) {  // a walked decision left the argmax path: re-add from the checkpoint
+              double acc = s.ck[fs >> 5];
+              for (int u = fs & ~31; u < n; ++u) acc = __dadd_rn(acc, static_cast<double>(s.o_lp[u]));
+              am = acc;
+            }
+          }
+          s.dsum[0] = am;
         }
-        s.dsum[0] = am;
       }
       if (boost && wid == 0) {
         // boost += the emitted frames' deltas in frame order (+ 0.0 for the
-        // others is the identity).  When every value (and the carry) is a
-        // multiple of 2^e and the sum of their magnitudes is below 2^(53+e),
-        // every partial sum in any order is exact in fp64, so the warp may
-        // add them as a tree and match the sequential sum bit for bit; the
-        // deltas are f32 scores of modest size, so this is the normal case.
-        // Otherwise one lane adds them sequentially.
+        // others is the identity): exact warp tree sum, else sequential
         const double carry = s.dsum[1];
-        double part = 0.0, sabs = 0.0;
-        int emin = INT_MAX;
-        for (int f = lane; f < n; f += 32) {
-          if (s.o_tok[f] < 0) continue;
-          const float d = s.o_s[f];
-          if (d == 0.0f) continue;
-          int e;
-          frexpf(d, &e);
-          emin = min(emin, max(e - 24, -149));
-          part = __dadd_rn(part, static_cast<double>(d));
-          sabs = __dadd_rn(sabs, fabs(static_cast<double>(d)));
-        }
-        if (carry != 0.0) {
-          int e;
-          frexp(carry, &e);
-          if (lane == 0) {
-            emin = min(emin, e - 53);
-            sabs = __dadd_rn(sabs, fabs(carry));
-          }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          part = __dadd_rn(part, __shfl_xor_sync(kFull, part, o));
-          sabs = __dadd_rn(sabs, __shfl_xor_sync(kFull, sabs, o));
-          emin = min(emin, __shfl_xor_sync(kFull, emin, o));
-        }
-        const bool exact = emin == INT_MAX || (emin > -1000 && sabs * (1.0 + 1e-12) < ldexp(1.0, 53 + emin));
+        int f = lane;
+        double tree;
+        const bool exact = exact_warp_sum(carry, [&](float &v) {
+          while (f < n && s.o_tok[f] < 0) f += 32;
+          if (f >= n) return false;
+          v = s.o_s[f];
+          f += 32;
+          return true;
+        }, tree);
         if (lane == 0) {
           if (exact) {
-            s.dsum[1] = __dadd_rn(carry, part);
+            s.dsum[1] = tree;
           } else {
             double acc = carry;
-            for (int f = 0; f < n; ++f)
-              if (s.o_tok[f] >= 0) acc = __dadd_rn(acc, static_cast<double>(s.o_s[f]));
+            for (int u = 0; u < n; ++u)
+              if (s.o_tok[u] >= 0) acc = __dadd_rn(acc, static_cast<double>(s.o_s[u]));
             s.dsum[1] = acc;
           }
         }

@@ -208,3 +208,20 @@ def test_boost_sum_fallback_wide_dynamic_range(t20k):
     got = _run(lps, None, tab, 1.0)
     _check(got, lps, None, tab, 1.0)
     assert any(abs(r.boost_score) > 1e5 for r in got)
+
+
+@pytest.mark.parametrize("lam", [0.0, 1.0])
+def test_am_sum_fallback_mixed_confidence(t20k, lam):
+    """Near-certain frames (argmax log-prob ~ -1e-15) mixed with flat ones
+    (~ -5): the log-probs span more than 53 bits, so the walker's exact tree
+    sum of am must fall back to the sequential fp64 sum (bit-exact)."""
+    phrases, V, tab = t20k
+    rng = np.random.default_rng(39)
+    B, T = 16, 250
+    logits = rng.normal(0.0, 2.0, size=(B, T, V))
+    peaky = rng.random((B, T)) < 0.3
+    idx = rng.integers(0, V, size=(B, T))
+    logits[peaky, idx[peaky]] += 45.0
+    lps = gi.log_softmax(logits).astype(np.float32)
+    lens = rng.integers(T // 2, T + 1, size=B).astype(np.int32)
+    _check(_run(lps, lens, tab, lam), lps, lens, tab, lam)
