@@ -225,3 +225,17 @@ def test_am_sum_fallback_mixed_confidence(t20k, lam):
     lps = gi.log_softmax(logits).astype(np.float32)
     lens = rng.integers(T // 2, T + 1, size=B).astype(np.int32)
     _check(_run(lps, lens, tab, lam), lps, lens, tab, lam)
+
+
+@pytest.mark.parametrize("seq", ["0", "1"])
+def test_vocab_4096_general_phase_a(seq):
+    """V=4096 (the AED vocabulary): phase A's multi-tile path and the walker's
+    48 KB shared root row, 20K-phrase tree."""
+    phrases, V = gi.corpus("p20k_v4096")
+    tab = product_table(phrases, V)
+    rng = np.random.default_rng(40)
+    B, T = 6, 160
+    lps = np.stack([_phrase_emissions(rng, phrases, T, V) for _ in range(B)])
+    lens = rng.integers(1, T + 1, size=B).astype(np.int32)
+    for lam in (0.0, 1.0):
+        _check(_run(lps, lens, tab, lam, {"PGPB_CTC_SEQ": seq}), lps, lens, tab, lam)
