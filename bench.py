@@ -362,10 +362,48 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
             if name == "boosted":
                 res["emitted_per_utt"] = float(o.num_out.double().mean().item())
         res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
+        if rank == 0 and regime in ("clean", "dense"):
+            res["cpu_reference"] = cpu_ctc_reference(lp[: min(B, 32)].cpu().numpy(), tab, B, T)
         out[regime] = res
         del lp
     out["_launches"] = launches
     return out
+
+
+def cpu_ctc_reference(lps, tab, B, T, budget_s=2.0):
+    """The reference's compiled greedy CTC kernel (oracle/_ref, _kernels.pyx:
+    75-225; the oracle port when absent) on the host cores, boosted, on a
+    bounded sample of the batch's utterances: 1 thread and all threads (the
+    kernel releases the GIL, as the reference CLI's --workers pool uses it)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as orc
+
+    mod, kind = _ref_module()
+    arrs = orc._tab_arrays(tab)
+    utts = [np.ascontiguousarray(x) for x in lps]
+
+    def one(x):
+        if mod is not None:
+            return mod.ctc_greedy(x, 0, 1.0, True, *arrs)
+        return orc.ctc_greedy(x, 0, 1.0, True, tab)
+
+    def per_utt(threads):
+        n, t0 = 0, time.perf_counter()
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            while True:
+                list(ex.map(one, utts))
+                n += len(utts)
+                if time.perf_counter() - t0 > budget_s:
+                    break
+        return (time.perf_counter() - t0) / n
+
+    threads = os.cpu_count() or 1
+    one(utts[0])
+    t1, tn = per_utt(1), per_utt(threads)
+    return {"kind": kind, "sample": f"{len(utts)} utterances of the batch, repeated for ~{budget_s:.0f} s",
+            "ms_per_batch_1thread": t1 * B * 1e3, "ms_per_batch": tn * B * 1e3, "cores": threads,
+            "rtfx": T * FRAME_SEC / tn, "rtfx_1thread": T * FRAME_SEC / t1}
 
 
 def bench_device_beams(dev, rank, world):
@@ -598,9 +636,17 @@ def cpu_baseline(tab, B, V, budget_s=10.0):
         _cpu_advance(tab, st, threads)
         n += 1
     el = time.perf_counter() - t0
+    # single-thread figure on a quarter batch (report both)
+    sub = st[: max(1, B // 4)]
+    n1, t1 = 0, time.perf_counter()
+    while time.perf_counter() - t1 < budget_s / 4:
+        _cpu_advance(tab, sub, 1)
+        n1 += 1
+    el1 = time.perf_counter() - t1
     return {"value": n * B * V / el, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{n} full advances of {B} states x V={V} (20K tree) in {el:.1f}s, "
                       f"batch sharded over {threads} threads",
+            "value_1thread": n1 * sub.shape[0] * V / el1,
             "cpu_model": _cpu_model()}
 
 

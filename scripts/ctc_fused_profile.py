@@ -37,5 +37,6 @@ for name, lp in cr.regimes(B, T, V, torch.device("cuda")).items():
         if lam:
             print("  steps(cyc):", [int(v) for v in buf[16:16 + 60]])
             print("  emit/need :", [int(v) for v in buf[128:128 + 60]])
-            print("  staged", int(buf[248]), "guess done per warp", [int(v) for v in buf[244:248]],
-                  "round0 done per warp", [int(v) for v in buf[240:244]])
+            print("  timeline: staged", int(buf[200]), "accountant", int(buf[201]), "guess", [int(v) for v in buf[210:214]],
+                  "round0", [int(v) for v in buf[220:224]], "walk done", int(buf[230]), "boost sum", int(buf[231]),
+                  "tail end", int(buf[8]))
