@@ -29,9 +29,10 @@
 //           within one emission and one fix-up round suffices; when boosting
 //           flips most decisions the fix-ups degrade to sequential walks,
 //           which then use the whole warp per step.
-//           Tail: am / boost summed in frame order in fp64 by one thread (the
-//           reference's rounding sequence), emitted frames compacted by a
-//           block scan.  Long utterances run in segments whose exact end
+//           Tail: am / boost as exact grid sums (every partial sum
+//           representable, checked, so equal to the reference's frame-order
+//           fp64 sums) with a sequential fallback; emitted frames compacted
+//           by a block scan.  Long utterances run in segments whose exact end
 //           state seeds the next segment's first chunk.
 //
 // Rerank at (state, frame) by one lane: the state's blob (header + closure
@@ -70,7 +71,19 @@ namespace cw {
 __device__ unsigned long long g_cf_prof[256];
 #define CF_COUNT(i, n) \
   do { if (blockIdx.x == 0) atomicAdd(&g_cf_prof[i], (unsigned long long)(n)); } while (0)
+// CTA-0 timeline: [200+i] = max over threads of cycles since kernel entry
+#define CF_MARK(i)                                                                                  \
+  do {                                                                                              \
+    if (blockIdx.x == 0 && int(threadIdx.x >> 5) < W) { /* walker warps only */                      \
+      const unsigned m_ = __activemask();                                                           \
+      const unsigned v_ = __reduce_max_sync(m_, unsigned(clock64() - t_entry));                     \
+      if ((threadIdx.x & 31) == __ffs(m_) - 1) atomicMax(&g_cf_prof[200 + (i) + 20 * cf_rep], (unsigned long long)v_); \
+    }                                                                                               \
+  } while (0)
 #else
+#define CF_MARK(i) \
+  do {             \
+  } while (0)
 #define CF_COUNT(i, n) \
   do {                 \
   } while (0)
@@ -80,6 +93,44 @@ constexpr int kMaxConsumers = 4;
 constexpr int kLaneArcs = 31;   // lane decisions up to 31 closure arcs (header + 31 = 512 B), larger -> warp
 
 constexpr int kSmemBudget = 96 * 1024;
+
+// Table reads of the walker carry an L2 evict-last hint: the tree's hot
+// lines (depth-1 states, their bitmaps) outlive phase A's evict-first stream
+// of log-probs, so the next call's dependent round trips hit L2.
+#ifndef PGPB_NO_L2_HINT
+__device__ __forceinline__ uint64_t el_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int4 tab_ld(const int4 *a) {
+  int4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(a), "l"(el_policy()));
+  return v;
+}
+__device__ __forceinline__ int tab_ld(const int *a) {
+  int v;
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(el_policy()));
+  return v;
+}
+__device__ __forceinline__ uint2 tab_ld(const uint2 *a) {
+  uint2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(a), "l"(el_policy()));
+  return v;
+}
+__device__ __forceinline__ uint32_t tab_ld(const uint32_t *a) {
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(el_policy()));
+  return v;
+}
+#else
+template <typename P>
+__device__ __forceinline__ P tab_ld(const P *a) {
+  return __ldg(a);
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // Phase A
@@ -260,6 +311,9 @@ struct Args {
   int use_boost;
   int TS;        // frames per segment
   int seq_mode;  // 0 auto, 1 always sequential, 2 never
+  int tlb_warm;  // touch every 2 MiB page of the table (and this utterance's rows) before walking
+  int stop;      // timing experiments only (PGPB_CTC_STOP): return after stage `stop` (outputs invalid)
+  int exp;       // timing experiments only (PGPB_CTC_EXP)
   int32_t *tokens;
   double *deltas;
   int32_t *ostates;
@@ -277,9 +331,10 @@ struct Smem {
   int32_t *c_soff, *c_slast, *c_eoff, *c_elast, *c_act, *c_sst, *c_est;  // [C]
   int32_t *misc;  // [0] seg start off, [1] seg start last, [2] emitted so far, [3] seg start state,
                   // [4] first frame whose walked log-prob differs from its argmax's
-  double *ck;     // am before frames 0, 32, 64, ... of the segment (accountant warp)
   double *dsum;   // [0] am, [1] boost: running totals across segments
   int32_t *wsum;  // [33] scan scratch
+  double *wred;   // [warp][4] tail partials: am sum, am |sum|, boost sum, boost |sum|
+  int32_t *wmin;  // [warp][4] tail minima: am grid exponent, boost grid exponent
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -317,9 +372,10 @@ __host__ __device__ inline size_t smem_bytes(int Vp, int Vw, int W, int TS, int 
   PGPB_TAKE(c_sst, int32_t, cb);
   PGPB_TAKE(c_est, int32_t, cb);
   PGPB_TAKE(misc, int32_t, 8 * 4);
-  PGPB_TAKE(ck, double, (size_t(TS) / 32 + 2) * 8);
   PGPB_TAKE(dsum, double, 2 * 8);
   PGPB_TAKE(wsum, int32_t, 33 * 4);
+  PGPB_TAKE(wred, double, 4 * 8 * (kMaxConsumers + 1));
+  PGPB_TAKE(wmin, int32_t, 4 * 4 * (kMaxConsumers + 1));
 #undef PGPB_TAKE
   return o;
 }
@@ -330,8 +386,10 @@ struct Ctx {
   const float *rows;  // row of local frame f at rows + f * V
   int V, blank;
   double lam;
+  double inv_lam;  // 1 / lam (filter thresholds only; decisions use fuse())
   float max_root;
   int lane;
+  int exp;  // timing experiments (PGPB_CTC_EXP)
 };
 
 // Dense candidates among {a, t2} and the frontier token of the bound: every
@@ -395,6 +453,7 @@ __device__ __forceinline__ bool lane_decide(const Ctx &x, const float *row, int 
       g_ld_rec[i][3] = threadIdx.x;
     }
   }
+  atomicAdd(&g_cf_prof[160 + 2 * path + (r ? 1 : 0)], 1ull);
   return r;
 #else
   int path = 0;
@@ -403,43 +462,55 @@ __device__ __forceinline__ bool lane_decide(const Ctx &x, const float *row, int 
 }
 __device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row, int off, int st, int last, int a,
                                                  float lpa, int t2, float lp2, BCand &out, int &path) {
-  const int4 *blob = x.t->blob + off;
-  const int4 h = __ldg(blob);
+  const int4 *blob = x.t->blob + off;  // (non-const: timing experiment 2)
   const float *root = x.s->root;
+  if (st == 0) {
+    path = 5;
+    // At the root the closure is the root row itself (shared memory): every
+    // token scores acc + root[v] with acc = 0 and moves to rnext[v], so the
+    // dense candidates {a, t2} and the frontier bound decide without a load.
+    BCand best = bcand_none();
+    bcand_consider(best, fuse(lpa, x.lam, root[a]), lpa, a, root[a], -1, 0);
+    const bool amax = root[a] == x.max_root;
+    if (!amax && t2 < x.V && t2 != x.blank && t2 != last)
+      bcand_consider(best, fuse(lp2, x.lam, root[t2]), lp2, t2, root[t2], -1, 0);
+    if (!certified(x, best, 0.0f, amax ? a : t2, amax ? lpa : lp2)) return false;
+    out = best;
+    out.nx = x.s->rnext[best.v];
+    out.noff = x.s->rnoff[best.v];
+    return true;
+  }
+  // timing experiments (decisions invalid): 1 no table loads, 2 loads confined
+  // to the first 1 MiB of the blob / 1024 bitmap rows, 3 header load only
+  const bool nold = x.exp == 1;
+  if (x.exp == 2) {
+    blob = x.t->blob + (off & 0xffff);
+    st &= 1023;
+  }
+  const int4 h = nold ? make_int4(0, 0, 0, __float_as_int(-INFINITY)) : tab_ld(blob);
   if (x.t->clo_bits) {
     // Fast path, one round trip: neither a nor t2 is a closure token and no
     // closure arc scores high enough to beat the dense winner.
-    const uint32_t *wb = x.t->clo_bits + int64_t(st) * x.t->bits_words;
-    const uint32_t wa = __ldg(wb + (a >> 5));
-    const uint32_t wt = t2 < x.V ? __ldg(wb + (t2 >> 5)) : 0u;
-    const bool a_in = (wa >> (a & 31)) & 1u, t2_in = t2 < x.V && ((wt >> (t2 & 31)) & 1u);
+    const uint2 *wb = x.t->clo_bits + int64_t(st) * x.t->bits_words;
+    const uint2 z2 = make_uint2(0u, 0u);
+    const uint2 wa = (nold || x.exp == 3) ? z2 : tab_ld(wb + (a >> 5));
+    const uint2 wt = (nold || x.exp == 3) ? z2 : (t2 < x.V ? tab_ld(wb + (t2 >> 5)) : z2);
+    const bool a_in = x.exp != 4 && ((wa.x >> (a & 31)) & 1u),
+               t2_in = x.exp != 4 && t2 < x.V && ((wt.x >> (t2 & 31)) & 1u);
     if (a_in || t2_in) {
+      path = 3;
       // Semi-fast path: a and/or t2 are closure tokens.  Their arcs are
-      // found by binary search over the token-sorted arcs (a few L1 hits);
+      // one load away (bitmap rank);
       // every other arc ranks after t2 and scores at most smax (header), so
       // when smax clears the crossing point of the bound the {a, t2}
       // candidates decide exactly, without scanning the closure.
-      const int count = h.x;
       const float acc = __int_as_float(h.y), smax = __int_as_float(h.w);
-      auto find = [&](int v, int4 &hit) {
-        int lo = 0, hi = count - 1;
-        while (lo <= hi) {
-          const int mid = (lo + hi) >> 1;
-          const int4 e = __ldg(blob + 1 + mid);
-          if (e.x == v) {
-            hit = e;
-            return true;
-          }
-          if (e.x < v)
-            lo = mid + 1;
-          else
-            hi = mid - 1;
-        }
-        return false;
+      // the entry's index = the word's rank + closure tokens below v in it
+      auto entry = [&](int v, uint2 w) {
+        return tab_ld(blob + 1 + int(w.y) + __popc(w.x & ((1u << (v & 31)) - 1u)));
       };
-      int4 ea = make_int4(0, 0, 0, 0), et = make_int4(0, 0, 0, 0);
-      if (a_in) find(a, ea);
-      if (t2_in) find(t2, et);
+      const int4 ea = a_in ? entry(a, wa) : make_int4(0, 0, 0, 0);
+      const int4 et = t2_in ? entry(t2, wt) : make_int4(0, 0, 0, 0);
       BCand best = bcand_none();
       int fid;
       float flp;
@@ -465,7 +536,7 @@ __device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row,
         }
       }
       if (x.lam > 0.0 && isfinite(best.c) && isfinite(lp2)) {
-        const double sx = (best.c - static_cast<double>(lp2)) / x.lam;
+        const double sx = (best.c - static_cast<double>(lp2)) * x.inv_lam;  // threshold only: the margin covers the rounding
         const float s_lo = static_cast<float>(sx - (fabs(sx) * 1e-6 + 1e-6));
         if (smax < s_lo && certified(x, best, acc, fid, flp)) {
           out = best;
@@ -485,7 +556,7 @@ __device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row,
         bcand_consider(best, fuse(lp2, x.lam, s2), lp2, t2, s2, -1, 0);
       }
       if (x.lam > 0.0 && isfinite(best.c) && isfinite(lp2)) {
-        const double sx = (best.c - static_cast<double>(lp2)) / x.lam;
+        const double sx = (best.c - static_cast<double>(lp2)) * x.inv_lam;  // threshold only: the margin covers the rounding
         const float s_lo = static_cast<float>(sx - (fabs(sx) * 1e-6 + 1e-6));
         path = 1;
         if (smax < s_lo && certified(x, best, acc, fid, flp)) {
@@ -498,11 +569,12 @@ __device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row,
       }
     }
   }
+  path += 8;
   int tok[kLaneArcs];
   float sc[kLaneArcs];
 #pragma unroll
   for (int j = 0; j < kLaneArcs; ++j) {  // blob is padded: safe past the end
-    const int4 e = __ldg(blob + 1 + j);
+    const int4 e = tab_ld(blob + 1 + j);
     tok[j] = e.x;
     sc[j] = __int_as_float(e.z);
   }
@@ -545,7 +617,7 @@ __device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row,
   // the crossing point minus a margin far above the fp64 rounding error).
   float s_lo = -INFINITY;
   if (x.lam > 0.0 && isfinite(best.c) && isfinite(lp2)) {
-    const double sx = (best.c - static_cast<double>(lp2)) / x.lam;
+    const double sx = (best.c - static_cast<double>(lp2)) * x.inv_lam;  // threshold only: the margin covers the rounding
     s_lo = static_cast<float>(sx - (fabs(sx) * 1e-6 + 1e-6));
   }
   bool surv[kLaneArcs];
@@ -566,7 +638,7 @@ __device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row,
   if (!certified(x, best, acc, fid, flp)) return false;
   out = best;
   if (best.nx >= 0) {  // winner is an arc: its successor from the blob (L1 hit)
-    const int4 e = __ldg(blob + 1 + best.nx);
+    const int4 e = tab_ld(blob + 1 + best.nx);
     out.nx = e.y;
     out.noff = e.w;
   } else {
@@ -587,13 +659,16 @@ __device__ BCand warp_decide(const Ctx &x, unsigned *bm, const float *row, int o
                              float lp2) {
   const int lane = x.lane;
   const int4 *blob = x.t->blob + off;
-  const int4 h = __ldg(blob);
-  const int4 e0 = __ldg(blob + 1 + lane);  // same round trip as the header (blob is padded)
+  const int4 h = tab_ld(blob);
+  const int4 e0 = tab_ld(blob + 1 + lane);  // same round trip as the header (blob is padded)
   const int count = h.x;
   const float acc = __int_as_float(h.y);
   const float *root = x.s->root;
   const int32_t *rnext = x.s->rnext, *rnoff = x.s->rnoff;
   if (lane == 0) CF_COUNT(3, 1);
+#ifdef PGPB_SEQ_PROFILE
+  if (lane == 0) atomicAdd(&g_cf_prof[192], 1ull);
+#endif
   BCand w;
   int fid;
   float flp;
@@ -640,7 +715,7 @@ __device__ BCand warp_decide(const Ctx &x, unsigned *bm, const float *row, int o
     BCand mine = bcand_none();
     bool a_l = false, t2_l = false;
     for (int i = lane; i < count; i += 32) {
-      const int4 e = i == lane ? e0 : __ldg(blob + 1 + i);
+      const int4 e = i == lane ? e0 : tab_ld(blob + 1 + i);
       if (e.x == a) {
         a_l = true;
         const float sv = __int_as_float(e.z);
@@ -663,7 +738,7 @@ __device__ BCand warp_decide(const Ctx &x, unsigned *bm, const float *row, int o
     }
     const BCand b1 = bcand_warp_best(mine);
     for (int i = lane; i < count; i += 32) {
-      const int4 e = __ldg(blob + 1 + i);  // L1 hit
+      const int4 e = tab_ld(blob + 1 + i);  // L1 hit
       if (e.x == a || e.x == t2 || e.x == x.blank || e.x == last) continue;
       const float sv = __int_as_float(e.z);
       if (!may_win(x, b1, sv, t2, lp2)) continue;
@@ -674,9 +749,12 @@ __device__ BCand warp_decide(const Ctx &x, unsigned *bm, const float *row, int o
   }
   if (certified(x, w, acc, fid, flp)) return w;
   if (lane == 0) CF_COUNT(4, 1);
+#ifdef PGPB_SEQ_PROFILE
+  if (lane == 0) atomicAdd(&g_cf_prof[193], 1ull);
+#endif
   // full rescan: every dense token, then the closure arcs
   for (int i = lane; i < count; i += 32) {
-    const int tok = __ldg(&blob[1 + i].x);
+    const int tok = tab_ld(&blob[1 + i].x);
     atomicOr(bm + (tok >> 5), 1u << (tok & 31));
   }
   __syncwarp();
@@ -688,7 +766,7 @@ __device__ BCand warp_decide(const Ctx &x, unsigned *bm, const float *row, int o
     bcand_consider(full, fuse(lv, x.lam, s), lv, v, s, rnext[v], rnoff[v]);
   }
   for (int i = lane; i < count; i += 32) {
-    const int4 e = __ldg(blob + 1 + i);
+    const int4 e = tab_ld(blob + 1 + i);
     if (e.x == x.blank || e.x == last) continue;
     const float lv = __ldg(row + e.x);
     const float sv = __int_as_float(e.z);
@@ -696,7 +774,7 @@ __device__ BCand warp_decide(const Ctx &x, unsigned *bm, const float *row, int o
   }
   w = bcand_warp_best(full);
   __syncwarp();
-  for (int i = lane; i < count; i += 32) bm[__ldg(&blob[1 + i].x) >> 5] = 0u;
+  for (int i = lane; i < count; i += 32) bm[tab_ld(&blob[1 + i].x) >> 5] = 0u;
   __syncwarp();
   return w;
 }
@@ -832,41 +910,47 @@ __device__ void seq_walk(const Ctx &x, unsigned *bm, int n, int &off, int &st, i
   __syncwarp();
 }
 
-// Exact warp sum of f32 values added to a fp64 carry.  When every value
+// Exact sum of f32 values and a fp64 carry in any order.  When every value
 // (and the carry) is a multiple of 2^e and the sum of their magnitudes is
 // below 2^(53+e), every partial sum in any order is representable in fp64,
-// so a tree sum equals the reference's sequential sum bit for bit; returns
-// false (and no sum) otherwise.  Call with all 32 lanes; lane l passes the
-// values it owns through `next(i)` for i = 0, 1, ... until it returns false.
-template <typename Next>
-__device__ __forceinline__ bool exact_warp_sum(double carry, Next next, double &out) {
+// so a tree sum equals the reference's sequential sum bit for bit;
+// exact_with() reports false (and no sum) otherwise.
+struct GridSum {
   double part = 0.0, sabs = 0.0;
-  int emin = INT_MAX;
-  float d;
-  while (next(d)) {
-    if (d == 0.0f) continue;
-    int e;
-    frexpf(d, &e);
-    emin = min(emin, max(e - 24, -149));
+  int emin = INT_MAX;  // smallest ulp exponent seen
+  __device__ __forceinline__ void add(float d) {
+    if (d == 0.0f) return;
+    const int be = (__float_as_int(d) >> 23) & 0xff;
+    emin = min(emin, be ? be - 150 : -149);
     part = __dadd_rn(part, static_cast<double>(d));
     sabs = __dadd_rn(sabs, fabs(static_cast<double>(d)));
   }
-  if (carry != 0.0 && (threadIdx.x & 31) == 0) {
-    int e;
-    frexp(carry, &e);
-    emin = min(emin, e - 53);
-    sabs = __dadd_rn(sabs, fabs(carry));
+  __device__ __forceinline__ void merge(double p, double a, int e) {
+    part = __dadd_rn(part, p);
+    sabs = __dadd_rn(sabs, a);
+    emin = min(emin, e);
   }
+  __device__ __forceinline__ void warp_reduce() {
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    part = __dadd_rn(part, __shfl_xor_sync(kFull, part, o));
-    sabs = __dadd_rn(sabs, __shfl_xor_sync(kFull, sabs, o));
-    emin = min(emin, __shfl_xor_sync(kFull, emin, o));
+    for (int o = 16; o; o >>= 1) {
+      part = __dadd_rn(part, __shfl_xor_sync(kFull, part, o));
+      sabs = __dadd_rn(sabs, __shfl_xor_sync(kFull, sabs, o));
+    }
+    emin = __reduce_min_sync(kFull, emin);
   }
-  const bool exact = emin == INT_MAX || (emin > -1000 && sabs * (1.0 + 1e-12) < ldexp(1.0, 53 + emin));
-  out = __dadd_rn(carry, part);
-  return exact;
-}
+  __device__ __forceinline__ bool exact_with(double carry, double &out) const {
+    int e = emin;
+    double a = sabs;
+    if (carry != 0.0) {
+      const int be = int((__double_as_longlong(carry) >> 52) & 0x7ff);
+      e = min(e, be ? be - 1075 : -1074);
+      a = __dadd_rn(a, fabs(carry));
+    }
+    if (!(e == INT_MAX || (e > -1000 && a * (1.0 + 1e-12) < ldexp(1.0, 53 + e)))) return false;
+    out = __dadd_rn(carry, part);
+    return true;
+  }
+};
 
 // Named barrier + OR over the CTA (all warps walk).
 __device__ __forceinline__ bool cta_or(bool pred) { return __syncthreads_or(pred) != 0; }
@@ -877,6 +961,10 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
   const int V = g.V, Vp = (V + 3) & ~3, Vw = (V + 31) >> 5;
   const int W = (blockDim.x >> 5) - 1, C = 32 * W, TS = g.TS;  // walker warps + 1 accountant warp
   const bool boost = g.use_boost != 0;
+#ifdef PGPB_SEQ_PROFILE
+  long long t_entry = clock64();
+  int cf_rep = 0;
+#endif
   Smem s;
   smem_bytes(Vp, Vw, W, TS, g.use_boost, &s, smem_raw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -890,8 +978,22 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
     for (int i = threadIdx.x; i < W * Vw; i += nthreads) s.bm[i] = 0u;
   }
   const int root_off = boost ? __ldg(t.blob_off) : 0;
+  // Address-translation warm-up: the walk's first dependent loads land on
+  // random pages of the table right after phase A streamed every page of
+  // the log-probs through the translation caches; one touch per 2 MiB page,
+  // issued with no consumer, overlaps the refill with the staging loads.
+  auto warm = [&]() {
+    if (!(boost && g.tlb_warm)) return;
+    for (int64_t o = int64_t(threadIdx.x) << 21; o < t.arena_bytes; o += int64_t(nthreads) << 21)
+      asm volatile("{ .reg .u32 t; ld.global.nc.u32 t, [%0]; }" ::"l"(t.arena + o));
+  };
+  warm();
   // programmatic dependent launch: the prologue above overlaps phase A's tail
+  CF_MARK(0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  CF_MARK(1);
+  warm();
+  if (g.stop == 1) return;
   Ctx x;
   x.t = &t;
   x.s = &s;
@@ -899,14 +1001,22 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
   x.V = V;
   x.blank = g.blank;
   x.lam = g.lam;
+  x.inv_lam = g.lam > 0.0 ? 1.0 / g.lam : 0.0;
+  x.exp = g.exp;
   x.max_root = t.max_root_score;
   x.lane = lane;
   unsigned *bm = boost ? s.bm + wid * Vw : nullptr;
   const int c = threadIdx.x;  // chunk of this lane
 
   for (int64_t b = blockIdx.x; b < g.B; b += gridDim.x) {
+#ifdef PGPB_SEQ_PROFILE
+    if (b != blockIdx.x) {  // second utterance of this CTA: a timeline of its own (warm instruction caches)
+      __syncthreads();
+      t_entry = clock64() - 5000;
+      cf_rep = 1;
+    }
+#endif
     const int64_t Tb = g.lengths ? int64_t(__ldg(g.lengths + b)) : g.T;
-    double am = 0.0;  // accountant lane 0
     __syncthreads();
     if (threadIdx.x == 0) {
       s.misc[0] = root_off;
@@ -926,29 +1036,103 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
       const int Cn = (n + L - 1) / L;  // non-empty chunks
       const float *rows = g.lp + (b * g.T + s0) * int64_t(V);
       const int4 *top = g.top + b * g.T + s0;
-      for (int f = threadIdx.x; f < n; f += nthreads) {
-        const int4 r = __ldg(top + f);
-        s.fa[f] = r.x;
-        s.flpa[f] = __int_as_float(r.y);
-        if (boost) {
-          s.ft2[f] = r.z;
-          s.flp2[f] = __int_as_float(r.w);
+      for (int f0 = threadIdx.x; f0 < n; f0 += 4 * nthreads) {
+        int4 r[4];  // all loads in flight before the first store: one round trip
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (f0 + u * nthreads < n) r[u] = __ldg(top + f0 + u * nthreads);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int f = f0 + u * nthreads;
+          if (f < n) {
+            s.fa[f] = r[u].x;
+            s.flpa[f] = __int_as_float(r[u].y);
+            if (boost) {
+              s.ft2[f] = r[u].z;
+              s.flp2[f] = __int_as_float(r[u].w);
+            }
+          }
         }
       }
       __syncthreads();
-      if (threadIdx.x == 0) s.misc[4] = n;
-      bool seq = false;
+      CF_MARK(2);
+      if (g.stop == 2) return;
+      // One pass of every walker lane over its chunk: the argmax emissions
+      // (for the round-0 guesses) and the mode counts.
+      //
+      // Round-0 start guess of chunk c (exact when boosting does not flip a
+      // decision near the boundary and the last emission starts no phrase
+      // continuation): last = the previous frame's argmax, state = the AC
+      // step from the depth-1 state of the second most recent argmax
+      // emission v1 on the most recent one v2.  (v1, v2) before the chunk
+      // come from a warp scan over the chunks and a lane-parallel look back
+      // before the warp's first chunk.  The step's bitmap word (with its
+      // rank: v2's entry index when v2 is on the closure) is loaded here and
+      // consumed after the mode decision.
+      int gv1 = -1, gv2 = -1;
+      uint2 gw = make_uint2(0u, 0u);
+      bool gfar = false, seq = false;
       if (boost) {
-        // Boost-sensitive frames: may emit and the top-2 gap is within the
-        // typical gain of a first-hit arc.  Mostly sensitive -> sequential.
-        int cand = 0, sens = 0;
-        for (int f = threadIdx.x; f < n; f += nthreads) {
-          const int a = s.fa[f], ap = f ? s.fa[f - 1] : s.misc[1];
-          if (a != g.blank && a != ap) {
-            ++cand;
-            sens += (s.flpa[f] - s.flp2[f]) < static_cast<float>(g.lam) * t.typ_gain;
+        int e1 = -1, e2 = -1, cand = 0, sens = 0;
+        if (c < Cn) {
+          for (int f = c * L, fe = min(f + L, n); f < fe; ++f) {
+            const int a = s.fa[f], ap = f ? s.fa[f - 1] : s.misc[1];
+            if (a != g.blank && a != ap) {
+              e1 = e2;
+              e2 = a;
+              ++cand;
+              sens += (s.flpa[f] - s.flp2[f]) < static_cast<float>(g.lam) * t.typ_gain;
+            }
           }
         }
+        // exclusive scan of "last two emissions" over this warp's chunks
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int p1 = __shfl_up_sync(kFull, e1, o), p2 = __shfl_up_sync(kFull, e2, o);
+          if (lane >= o && e1 < 0) {
+            e1 = e2 >= 0 ? p2 : p1;
+            e2 = e2 >= 0 ? e2 : p2;
+          }
+        }
+        gv1 = __shfl_up_sync(kFull, e1, 1);
+        gv2 = __shfl_up_sync(kFull, e2, 1);
+        if (lane == 0) gv1 = gv2 = -1;
+        // emissions before the warp's first chunk: up to 64 frames back, 32 per ballot
+        const int cbw = (c & ~31) * L;
+        int w1 = -1, w2 = -1, fw0 = cbw;
+        if (wid >= W || cbw >= n) fw0 = 0;  // helper warp / no live chunk: nothing to look back for
+        for (; fw0 > 0 && fw0 > cbw - 64 && w1 < 0; fw0 -= 32) {
+          const int fw = fw0 - 1 - lane;
+          int at = -1;
+          bool em = false;
+          if (fw >= 0) {
+            at = s.fa[fw];
+            em = at != g.blank && at != (fw ? s.fa[fw - 1] : s.misc[1]);
+          }
+          unsigned m = __ballot_sync(kFull, em);
+          while (m && w1 < 0) {
+            const int v = __shfl_sync(kFull, at, __ffs(m) - 1);
+            m &= m - 1;
+            if (w2 < 0)
+              w2 = v;
+            else
+              w1 = v;
+          }
+        }
+        if (gv2 < 0) {
+          gv1 = w1;
+          gv2 = w2;
+        } else if (gv1 < 0) {
+          gv1 = w2;
+        }
+        gfar = gv2 < 0 && fw0 > 0;
+        CF_MARK(12);
+        if (c > 0 && c < Cn && gv1 >= 0 && t.clo_bits && s.rnext[gv1] != 0) {
+          gw = tab_ld(t.clo_bits + int64_t(s.rnext[gv1]) * t.bits_words + (gv2 >> 5));
+        }
+        CF_MARK(13);
+        // Boost-sensitive frames: may emit and the top-2 gap is within the
+        // typical gain of a first-hit arc.  Mostly sensitive -> sequential.
         cand = __reduce_add_sync(kFull, cand);
         sens = __reduce_add_sync(kFull, sens);
         if (lane == 0) {
@@ -962,36 +1146,9 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
           ts += s.wsum[16 + w];
         }
         seq = g.seq_mode == 1 || (g.seq_mode == 0 && 4 * ts > tc && tc >= 8);
-        __syncthreads();
+        CF_MARK(3);
       }
-      // Accountant warp: am = sum of the argmax log-probs in frame order (the
-      // reference's fp64 rounding sequence), with a checkpoint every 32
-      // frames, while the walkers decide.  Exact when unboosted; when
-      // boosted it is the final am unless a walked decision picked a token
-      // other than its frame's argmax (checked and repaired in the tail).
-      if (boost && wid == W && lane == 0) {  // (unboosted: the tail's exact tree sum, see below)
-#ifdef PGPB_SEQ_PROFILE
-        const long long t0 = clock64();
-#endif
-        double acc = s.dsum[0];
-        for (int f0 = 0; f0 < n; f0 += 32) {
-          s.ck[f0 >> 5] = acc;
-          const int e = min(f0 + 32, n);
-          int f = f0;
-          for (; f + 8 <= e; f += 8) {
-            float v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = s.flpa[f + u];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, static_cast<double>(v[u]));
-          }
-          for (; f < e; ++f) acc = __dadd_rn(acc, static_cast<double>(s.flpa[f]));
-        }
-        am = acc;
-#ifdef PGPB_SEQ_PROFILE
-        if (blockIdx.x == 0) CF_COUNT(13, clock64() - t0);
-#endif
-      }
+      if (g.stop == 3) return;
       if (boost && seq) {
         // ---- sequential mode: warp 0 walks the segment ----
         x.rows = rows;
@@ -1011,48 +1168,19 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         const int cb = c * L, ce = min(cb + L, n);
         int off = s.misc[0], st = s.misc[3], last = s.misc[1];
         if (c > 0 && live) {
-          // Guess (exact when boosting does not flip a decision near the
-          // boundary and the last emission starts no phrase continuation):
-          // last = the previous frame's argmax, state = the depth-1 state
-          // of the most recent argmax emission.
           last = s.fa[cb - 1];
-          // the two most recent argmax emissions v1, v2 (in that order)
-          int v1 = -1, v2 = -1;
-          const int lim = max(0, cb - 64);
-          for (int u = cb - 1; u >= lim && v1 < 0; --u) {
-            const int at = s.fa[u], ap = u ? s.fa[u - 1] : s.misc[1];
-            if (at != g.blank && at != ap) {
-              if (v2 < 0)
-                v2 = at;
-              else
-                v1 = at;
+          if (gv2 >= 0) {
+            off = s.rnoff[gv2];
+            st = s.rnext[gv2];
+            CF_MARK(14);
+            if ((gw.x >> (gv2 & 31)) & 1u) {
+              CF_COUNT(22, 1);
+              // v2 is on v1's state's closure: its entry by rank
+              const int4 e = tab_ld(t.blob + s.rnoff[gv1] + 1 + int(gw.y) + __popc(gw.x & ((1u << (gv2 & 31)) - 1u)));
+              off = e.w;
+              st = e.y;
             }
-          }
-          if (v2 >= 0) {
-            off = s.rnoff[v2];
-            st = s.rnext[v2];
-            if (v1 >= 0 && t.clo_bits) {
-              // AC step from the depth-1 state of v1 on v2: its first-hit arc, if any
-              const int s1 = s.rnext[v1];
-              if ((__ldg(t.clo_bits + int64_t(s1) * t.bits_words + (v2 >> 5)) >> (v2 & 31)) & 1u) {
-                // v2 is on s1's sorted arc list: two-level search (two round trips)
-                const int4 *b1 = t.blob + s.rnoff[v1] + 1;
-                const int cnt1 = __ldg(&b1[-1].x);
-                int seg = 0;
-#pragma unroll
-                for (int q = 1; q < 8; ++q) seg += (8 * q < cnt1 && __ldg(&b1[8 * q].x) <= v2);
-                int4 e8[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) e8[q] = __ldg(b1 + 8 * seg + q);  // blob is padded
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  if (8 * seg + q < cnt1 && e8[q].x == v2) {
-                    off = e8[q].w;
-                    st = e8[q].y;
-                  }
-              }
-            }
-          } else if (lim > 0) {
+          } else if (gfar) {
             off = root_off;
             st = 0;
           }
@@ -1060,6 +1188,11 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         s.c_soff[c] = off;
         s.c_sst[c] = st;
         s.c_slast[c] = last;
+        CF_MARK(4);
+        if (g.stop == 4) return;
+#ifdef PGPB_SEQ_PROFILE
+        const long long t_r0 = clock64();
+#endif
         for (int k = 0; k < L; ++k) {
           const int f = cb + k;
 #ifdef PGPB_SEQ_PROFILE
@@ -1073,6 +1206,16 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         s.c_eoff[c] = off;
         s.c_est[c] = st;
         s.c_elast[c] = last;
+        CF_MARK(5);
+        if (g.stop == 5) return;
+#ifdef PGPB_SEQ_PROFILE
+        if (lane == 0 && wid < W) {
+          const unsigned long long d = clock64() - t_r0;
+          atomicMax(&g_cf_prof[194], d);
+          atomicAdd(&g_cf_prof[195], d);
+          atomicAdd(&g_cf_prof[196], 1ull);
+        }
+#endif
 #ifdef PGPB_SEQ_PROFILE
         if (blockIdx.x == 0 && threadIdx.x == 0) CF_COUNT(6, clock64() - t_start);
 #endif
@@ -1149,91 +1292,45 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         }
       }
       __syncthreads();
-      // ---- tail: repair am if needed, boost sum, compaction ----
-      if (boost) {
-        for (int f = threadIdx.x; f < n; f += nthreads)
-          if (__float_as_int(s.o_lp[f]) != __float_as_int(s.flpa[f])) atomicMin(s.misc + 4, f);
-      }
-      __syncthreads();
-      if (wid == W) {
-        // am over every frame in order: the exact warp tree sum when it is
-        // exact (the usual case), else the accountant's sequential sum
-        // (boosted: computed during the walk and repaired from the first
-        // off-argmax frame; unboosted: computed here)
-        int f = lane;
-        double tree;
-        const bool exact = exact_warp_sum(s.dsum[0], [&](float &v) {
-          if (f >= n) return false;
-          v = s.o_lp[f];
-          f += 32;
-          return true;
-        }, tree);
-        if (lane == 0) {
-          if (exact) {
-            am = tree;
-          } else if (!boost) {
-            double acc = s.dsum[0];
-            for (int u = 0; u < n; ++u) acc = __dadd_rn(acc, static_cast<double>(s.o_lp[u]));
-            am = acc;
-          } else {
-            const int fs = s.misc[4];
-            if (fs < n) {  // a walked decision left the argmax path: re-add from the checkpoint
-              double acc = s.ck[fs >> 5];
-              for (int u = fs & ~31; u < n; ++u) acc = __dadd_rn(acc, static_cast<double>(s.o_lp[u]));
-              am = acc;
-            }
-          }
-          s.dsum[0] = am;
-        }
-      }
-      if (boost && wid == 0) {
-        // boost += the emitted frames' deltas in frame order (+ 0.0 for the
-        // others is the identity): exact warp tree sum, else sequential
-        const double carry = s.dsum[1];
-        int f = lane;
-        double tree;
-        const bool exact = exact_warp_sum(carry, [&](float &v) {
-          while (f < n && s.o_tok[f] < 0) f += 32;
-          if (f >= n) return false;
-          v = s.o_s[f];
-          f += 32;
-          return true;
-        }, tree);
-        if (lane == 0) {
-          if (exact) {
-            s.dsum[1] = tree;
-          } else {
-            double acc = carry;
-            for (int u = 0; u < n; ++u)
-              if (s.o_tok[u] >= 0) acc = __dadd_rn(acc, static_cast<double>(s.o_s[u]));
-            s.dsum[1] = acc;
-          }
-        }
-      }
-      // block exclusive scan of emit flags over n frames
+      CF_MARK(6);
+      if (g.stop == 6) return;
+      // ---- tail: one pass over each thread's contiguous frames (emit
+      // count, exact-sum partials of am and boost),
+      // warp scans / reductions, one barrier, then compaction ----
       const int q = (n + nthreads - 1) / nthreads;
       const int f0 = min(int(threadIdx.x) * q, n), f1 = min(f0 + q, n);
+      const int base = s.misc[2];
       int cntm = 0;
-      for (int f = f0; f < f1; ++f) cntm += s.o_tok[f] >= 0;
+      GridSum ga, gb;
+      for (int f = f0; f < f1; ++f) {
+        const int tk = s.o_tok[f];
+        const float lpv = s.o_lp[f];
+        cntm += tk >= 0;
+        ga.add(lpv);
+        if (boost && tk >= 0) gb.add(s.o_s[f]);
+      }
       int incl = cntm;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(kFull, incl, o);
         if (lane >= o) incl += y;
       }
+      ga.warp_reduce();
+      if (boost) gb.warp_reduce();
       if (lane == 31) s.wsum[wid] = incl;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int w = 0; w <= W; ++w) {
-          const int v = s.wsum[w];
-          s.wsum[w] = acc;
-          acc += v;
-        }
-        s.wsum[32] = acc;
+      if (lane == 0) {
+        s.wred[4 * wid] = ga.part;
+        s.wred[4 * wid + 1] = ga.sabs;
+        s.wred[4 * wid + 2] = gb.part;
+        s.wred[4 * wid + 3] = gb.sabs;
+        s.wmin[4 * wid] = ga.emin;
+        s.wmin[4 * wid + 1] = gb.emin;
       }
       __syncthreads();
-      int pos = s.misc[2] + s.wsum[wid] + incl - cntm;
+      CF_MARK(7);
+      if (g.stop == 7) return;
+      int pos = base + incl - cntm;
+      for (int w = 0; w < wid; ++w) pos += s.wsum[w];
       int32_t *otok = g.tokens + b * g.T;
       double *odl = g.deltas + b * g.T;
       int32_t *ost = g.ostates + b * g.T;
@@ -1246,9 +1343,34 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
           ++pos;
         }
       }
-      __syncthreads();
       if (threadIdx.x == 0) {
-        s.misc[2] += s.wsum[32];
+        // am / boost over every frame in order: the exact grid sum when it is
+        // exact (the usual case), else the reference's sequential order
+        GridSum ta, tb;
+        int tot = 0;
+        for (int w = 0; w <= W; ++w) {
+          ta.merge(s.wred[4 * w], s.wred[4 * w + 1], s.wmin[4 * w]);
+          tb.merge(s.wred[4 * w + 2], s.wred[4 * w + 3], s.wmin[4 * w + 1]);
+          tot += s.wsum[w];
+        }
+        double am;
+        if (!ta.exact_with(s.dsum[0], am)) {
+          double acc = s.dsum[0];
+          for (int u = 0; u < n; ++u) acc = __dadd_rn(acc, static_cast<double>(s.o_lp[u]));
+          am = acc;
+        }
+        s.dsum[0] = am;
+        if (boost) {
+          double bo;
+          if (!tb.exact_with(s.dsum[1], bo)) {
+            double acc = s.dsum[1];
+            for (int u = 0; u < n; ++u)
+              if (s.o_tok[u] >= 0) acc = __dadd_rn(acc, static_cast<double>(s.o_s[u]));
+            bo = acc;
+          }
+          s.dsum[1] = bo;
+        }
+        s.misc[2] = base + tot;
         if (boost) {
           s.misc[0] = s.c_eoff[Cn - 1];
           s.misc[1] = s.c_elast[Cn - 1];
@@ -1257,11 +1379,13 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
           s.misc[1] = s.fa[n - 1];
         }
       }
+      __syncthreads();
     }
     __syncthreads();
 #ifdef PGPB_SEQ_PROFILE
     if (blockIdx.x == 0 && threadIdx.x == 0) CF_COUNT(8, clock64() - t_start);
 #endif
+    CF_MARK(8);
     if (threadIdx.x == 0) {
       g.nout[b] = s.misc[2];
       g.am_out[b] = s.dsum[0];
@@ -1329,6 +1453,12 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
     return fail(PGPB_EINVAL, "vocabulary too large for the CTC walker's shared-memory root row");
   }
   a.TS = TS;
+  const char *et = getenv("PGPB_CTC_TLB");
+  a.tlb_warm = et ? atoi(et) != 0 : 1;
+  const char *ex = getenv("PGPB_CTC_STOP");
+  a.stop = ex ? atoi(ex) : 0;
+  const char *ee = getenv("PGPB_CTC_EXP");
+  a.exp = ee ? atoi(ee) : 0;
   const char *eq = getenv("PGPB_CTC_SEQ");
   a.seq_mode = eq ? std::max(0, std::min(2, atoi(eq))) : 0;
   if (smem > 48 * 1024) {

@@ -23,13 +23,20 @@
 namespace pgpb {
 
 // Successor of (off, st) on token w: the state's first-hit arc if w is on its
-// closure (bitmap test, then a binary search of the token-sorted arcs),
-// otherwise the root row.
+// closure (bitmap word; the entry's index is the word's rank plus the closure
+// tokens below w in it), otherwise the root row.  Without bitmaps: binary
+// search of the token-sorted arcs.
 __device__ __forceinline__ void ac_next(const TableView &t, int &off, int &st, int w) {
-  bool on = true;
-  if (t.clo_bits) on = (__ldg(t.clo_bits + int64_t(st) * t.bits_words + (w >> 5)) >> (w & 31)) & 1u;
-  if (on) {
-    const int4 *b = t.blob + off;
+  const int4 *b = t.blob + off;
+  if (t.clo_bits) {
+    const uint2 cw = __ldg(t.clo_bits + int64_t(st) * t.bits_words + (w >> 5));
+    if ((cw.x >> (w & 31)) & 1u) {
+      const int4 e = __ldg(b + 1 + cw.y + __popc(cw.x & ((1u << (w & 31)) - 1u)));
+      off = e.w;
+      st = e.y;
+      return;
+    }
+  } else {
     int lo = 0, hi = __ldg(&b->x) - 1;
     while (lo <= hi) {
       const int mid = (lo + hi) >> 1;

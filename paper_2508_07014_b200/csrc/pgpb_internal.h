@@ -41,12 +41,16 @@ struct TableView {
   const int32_t *blob_off;     // [S]
   const int32_t *root_next_off;  // [Vp] blob_off[root_next[v]]
   // Per state: bitmap of its closure tokens (Vw = ceil(V/32) words per
-  // state), so a decoder tests "is v a first-hit arc of s" with one load
-  // instead of a scan; NULL when S * Vw words would exceed the cap.  The
-  // blob header's 4th field holds the state's largest closure-arc score
-  // (bits of an f32, -inf when the closure is empty).
-  const uint32_t *clo_bits;    // [S][Vw]
+  // state), each word paired with the number of closure tokens below it, so
+  // a decoder tests "is v a first-hit arc of s" with one 8-byte load and,
+  // when it is, finds v's entry at blob[blob_off[s] + 1 + rank] (rank = the
+  // word's count + popc of the lower bits) without a search; NULL when
+  // S * Vw pairs would exceed the cap.  The blob header's 4th field holds the
+  // state's largest closure-arc score (bits of an f32, -inf when empty).
+  const uint2 *clo_bits;       // [S][Vw] {bits, closure tokens in words < w}
   int32_t bits_words;          // Vw
+  const unsigned char *arena;  // the whole table (address-translation warm-up of latency-bound walkers)
+  int64_t arena_bytes;
 };
 
 }  // namespace pgpb

@@ -136,17 +136,22 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
     }
     b[0] = make_int4(r.y, r.z, s0, f2i(smax));
   }
-  // Closure-token bitmaps (capped at 512 MiB).
+  // Closure-token bitmaps with per-word ranks (capped at 1 GiB).
   const int32_t Vw = (V + 31) / 32;
-  const bool with_bits = int64_t(S) * Vw * 4 <= (int64_t(512) << 20);
-  std::vector<uint32_t> bits(with_bits ? static_cast<size_t>(S) * Vw : 1, 0u);
+  const bool with_bits = int64_t(S) * Vw * 8 <= (int64_t(1) << 30);
+  std::vector<uint32_t> bits(with_bits ? static_cast<size_t>(S) * Vw * 2 : 2, 0u);
   if (with_bits)
     for (int32_t s0 = 0; s0 < S; ++s0) {
       const int4 r = clo_rec[s0];
-      uint32_t *w = bits.data() + static_cast<size_t>(s0) * Vw;
+      uint32_t *w = bits.data() + static_cast<size_t>(s0) * Vw * 2;
       for (int32_t i = 0; i < r.y; ++i) {
         const int32_t v = clo[static_cast<size_t>(r.x) + i].x;
-        w[v >> 5] |= 1u << (v & 31);
+        w[2 * (v >> 5)] |= 1u << (v & 31);
+      }
+      uint32_t below = 0;
+      for (int32_t k = 0; k < Vw; ++k) {
+        w[2 * k + 1] = below;
+        below += static_cast<uint32_t>(__builtin_popcount(w[2 * k]));
       }
     }
   std::vector<int32_t> rn_off(static_cast<size_t>(Vp), 0);
@@ -239,8 +244,10 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   v.blob = reinterpret_cast<const int4 *>(arena + o_blob);
   v.blob_off = reinterpret_cast<const int32_t *>(arena + o_boff);
   v.root_next_off = reinterpret_cast<const int32_t *>(arena + o_rno);
-  v.clo_bits = with_bits ? reinterpret_cast<const uint32_t *>(arena + o_bits) : nullptr;
+  v.clo_bits = with_bits ? reinterpret_cast<const uint2 *>(arena + o_bits) : nullptr;
   v.bits_words = Vw;
+  v.arena = reinterpret_cast<const unsigned char *>(arena);
+  v.arena_bytes = total;
   *out = t;
   return PGPB_OK;
 }

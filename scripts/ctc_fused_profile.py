@@ -37,6 +37,14 @@ for name, lp in cr.regimes(B, T, V, torch.device("cuda")).items():
         if lam:
             print("  steps(cyc):", [int(v) for v in buf[16:16 + 60]])
             print("  emit/need :", [int(v) for v in buf[128:128 + 60]])
-            print("  timeline: staged", int(buf[200]), "accountant", int(buf[201]), "guess", [int(v) for v in buf[210:214]],
-                  "round0", [int(v) for v in buf[220:224]], "walk done", int(buf[230]), "boost sum", int(buf[231]),
-                  "tail end", int(buf[8]))
+            print("  timeline (CTA 0, cycles since entry): prologue", int(buf[200]), "wait released", int(buf[201]),
+                  "staged", int(buf[202]), "mode", int(buf[203]), "guessed", int(buf[204]), "round0", int(buf[205]),
+                  "walk done", int(buf[206]), "sums", int(buf[207]), "end", int(buf[208]), "scanback", int(buf[212]), "rt1 issued", int(buf[213]), "rt1 used", int(buf[214]), "rt2 lanes", int(buf[22]))
+            names2 = {0: "none", 1: "fast", 3: "semi", 5: "root", 8: "scan", 9: "fast>scan", 11: "semi>scan"}
+            print("  lane paths (all CTAs):", {f"{names2.get(k, k)}:{'ok' if r else 'fail'}": int(buf[160 + 2 * k + r])
+                                               for k in range(16) for r in (0, 1) if buf[160 + 2 * k + r]})
+            print("  warp decisions", int(buf[192]), "rescans", int(buf[193]), "round0 per warp: max", int(buf[194]),
+                  "mean", int(buf[195]) / max(1, int(buf[196])))
+            print("  2nd utterance (entry = start - 5000):", [int(v) for v in buf[220:235]])
+            print("  latency: top", int(buf[240]), "blob", int(buf[241]), "top again", int(buf[242]), "bitmap", int(buf[243]),
+                  "| at the end: blob", int(buf[244]), "bitmap", int(buf[245]))
