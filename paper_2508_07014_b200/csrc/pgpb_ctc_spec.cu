@@ -89,7 +89,7 @@ __device__ unsigned long long g_cf_prof[256];
   } while (0)
 #endif
 
-constexpr int kMaxConsumers = 4;
+constexpr int kMaxConsumers = 7;  // walker warps (+1 helper warp): 256 threads
 constexpr int kLaneArcs = 31;   // lane decisions up to 31 closure arcs (header + 31 = 512 B), larger -> warp
 
 constexpr int kSmemBudget = 96 * 1024;
@@ -311,9 +311,7 @@ struct Args {
   int use_boost;
   int TS;        // frames per segment
   int seq_mode;  // 0 auto, 1 always sequential, 2 never
-  int tlb_warm;  // touch every 2 MiB page of the table (and this utterance's rows) before walking
   int stop;      // timing experiments only (PGPB_CTC_STOP): return after stage `stop` (outputs invalid)
-  int exp;       // timing experiments only (PGPB_CTC_EXP)
   int32_t *tokens;
   double *deltas;
   int32_t *ostates;
@@ -389,7 +387,6 @@ struct Ctx {
   double inv_lam;  // 1 / lam (filter thresholds only; decisions use fuse())
   float max_root;
   int lane;
-  int exp;  // timing experiments (PGPB_CTC_EXP)
 };
 
 // Dense candidates among {a, t2} and the frontier token of the bound: every
@@ -462,7 +459,7 @@ __device__ __forceinline__ bool lane_decide(const Ctx &x, const float *row, int 
 }
 __device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row, int off, int st, int last, int a,
                                                  float lpa, int t2, float lp2, BCand &out, int &path) {
-  const int4 *blob = x.t->blob + off;  // (non-const: timing experiment 2)
+  const int4 *blob = x.t->blob + off;
   const float *root = x.s->root;
   if (st == 0) {
     path = 5;
@@ -480,23 +477,14 @@ __device__ __forceinline__ bool lane_decide_impl(const Ctx &x, const float *row,
     out.noff = x.s->rnoff[best.v];
     return true;
   }
-  // timing experiments (decisions invalid): 1 no table loads, 2 loads confined
-  // to the first 1 MiB of the blob / 1024 bitmap rows, 3 header load only
-  const bool nold = x.exp == 1;
-  if (x.exp == 2) {
-    blob = x.t->blob + (off & 0xffff);
-    st &= 1023;
-  }
-  const int4 h = nold ? make_int4(0, 0, 0, __float_as_int(-INFINITY)) : tab_ld(blob);
+  const int4 h = tab_ld(blob);
   if (x.t->clo_bits) {
     // Fast path, one round trip: neither a nor t2 is a closure token and no
     // closure arc scores high enough to beat the dense winner.
     const uint2 *wb = x.t->clo_bits + int64_t(st) * x.t->bits_words;
-    const uint2 z2 = make_uint2(0u, 0u);
-    const uint2 wa = (nold || x.exp == 3) ? z2 : tab_ld(wb + (a >> 5));
-    const uint2 wt = (nold || x.exp == 3) ? z2 : (t2 < x.V ? tab_ld(wb + (t2 >> 5)) : z2);
-    const bool a_in = x.exp != 4 && ((wa.x >> (a & 31)) & 1u),
-               t2_in = x.exp != 4 && t2 < x.V && ((wt.x >> (t2 & 31)) & 1u);
+    const uint2 wa = tab_ld(wb + (a >> 5));
+    const uint2 wt = t2 < x.V ? tab_ld(wb + (t2 >> 5)) : make_uint2(0u, 0u);
+    const bool a_in = (wa.x >> (a & 31)) & 1u, t2_in = t2 < x.V && ((wt.x >> (t2 & 31)) & 1u);
     if (a_in || t2_in) {
       path = 3;
       // Semi-fast path: a and/or t2 are closure tokens.  Their arcs are
@@ -970,29 +958,36 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nthreads = blockDim.x;
   if (boost) {
-    for (int i = threadIdx.x; i < Vp; i += nthreads) {
-      s.root[i] = __ldg(t.root_scores + i);
-      s.rnext[i] = __ldg(t.root_next + i);
-      s.rnoff[i] = __ldg(t.root_next_off + i);
+    // root row -> shared memory, every load of a thread in flight at once
+    for (int i0 = threadIdx.x; i0 < Vp; i0 += 4 * nthreads) {
+      float r0[4];
+      int r1[4], r2[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nthreads;
+        if (i < Vp) {
+          r0[u] = __ldg(t.root_scores + i);
+          r1[u] = __ldg(t.root_next + i);
+          r2[u] = __ldg(t.root_next_off + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nthreads;
+        if (i < Vp) {
+          s.root[i] = r0[u];
+          s.rnext[i] = r1[u];
+          s.rnoff[i] = r2[u];
+        }
+      }
     }
     for (int i = threadIdx.x; i < W * Vw; i += nthreads) s.bm[i] = 0u;
   }
   const int root_off = boost ? __ldg(t.blob_off) : 0;
-  // Address-translation warm-up: the walk's first dependent loads land on
-  // random pages of the table right after phase A streamed every page of
-  // the log-probs through the translation caches; one touch per 2 MiB page,
-  // issued with no consumer, overlaps the refill with the staging loads.
-  auto warm = [&]() {
-    if (!(boost && g.tlb_warm)) return;
-    for (int64_t o = int64_t(threadIdx.x) << 21; o < t.arena_bytes; o += int64_t(nthreads) << 21)
-      asm volatile("{ .reg .u32 t; ld.global.nc.u32 t, [%0]; }" ::"l"(t.arena + o));
-  };
-  warm();
   // programmatic dependent launch: the prologue above overlaps phase A's tail
   CF_MARK(0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   CF_MARK(1);
-  warm();
   if (g.stop == 1) return;
   Ctx x;
   x.t = &t;
@@ -1002,7 +997,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
   x.blank = g.blank;
   x.lam = g.lam;
   x.inv_lam = g.lam > 0.0 ? 1.0 / g.lam : 0.0;
-  x.exp = g.exp;
   x.max_root = t.max_root_score;
   x.lane = lane;
   unsigned *bm = boost ? s.bm + wid * Vw : nullptr;
@@ -1437,8 +1431,8 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
   a.boost_out = d_boost;
   const int Vp = (V + 3) & ~3, Vw = (V + 31) >> 5;
   int W = use_boost ? 1 : kMaxConsumers;
-  if (use_boost) {  // about two frames per chunk in round 0
-    const int64_t want = (T + 63) / 64;
+  if (use_boost) {  // one frame per chunk in round 0 up to 224 frames per segment
+    const int64_t want = (T + 31) / 32;
     W = int(want < 1 ? 1 : (want > kMaxConsumers ? kMaxConsumers : want));
   }
   const char *ew = getenv("PGPB_CTC_CONSUMERS");
@@ -1453,12 +1447,8 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
     return fail(PGPB_EINVAL, "vocabulary too large for the CTC walker's shared-memory root row");
   }
   a.TS = TS;
-  const char *et = getenv("PGPB_CTC_TLB");
-  a.tlb_warm = et ? atoi(et) != 0 : 1;
   const char *ex = getenv("PGPB_CTC_STOP");
   a.stop = ex ? atoi(ex) : 0;
-  const char *ee = getenv("PGPB_CTC_EXP");
-  a.exp = ee ? atoi(ee) : 0;
   const char *eq = getenv("PGPB_CTC_SEQ");
   a.seq_mode = eq ? std::max(0, std::min(2, atoi(eq))) : 0;
   if (smem > 48 * 1024) {
@@ -1472,7 +1462,9 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctc_walk_kernel, 32 * (W + 1), smem);
   const int64_t cap = int64_t(sm_count(current_device())) * std::max(per_sm, 1);
-  const unsigned grid = unsigned(B < cap ? B : cap);
+  unsigned grid = unsigned(B < cap ? B : cap);
+  const char *eg = getenv("PGPB_CTC_GRID");  // timing experiments: cap the walker grid
+  if (eg && atoi(eg) > 0) grid = std::min(grid, unsigned(atoi(eg)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(32 * (W + 1));

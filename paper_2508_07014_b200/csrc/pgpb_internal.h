@@ -49,8 +49,6 @@ struct TableView {
   // state's largest closure-arc score (bits of an f32, -inf when empty).
   const uint2 *clo_bits;       // [S][Vw] {bits, closure tokens in words < w}
   int32_t bits_words;          // Vw
-  const unsigned char *arena;  // the whole table (address-translation warm-up of latency-bound walkers)
-  int64_t arena_bytes;
 };
 
 }  // namespace pgpb

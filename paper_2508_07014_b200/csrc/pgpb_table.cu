@@ -246,8 +246,6 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   v.root_next_off = reinterpret_cast<const int32_t *>(arena + o_rno);
   v.clo_bits = with_bits ? reinterpret_cast<const uint2 *>(arena + o_bits) : nullptr;
   v.bits_words = Vw;
-  v.arena = reinterpret_cast<const unsigned char *>(arena);
-  v.arena_bytes = total;
   *out = t;
   return PGPB_OK;
 }
