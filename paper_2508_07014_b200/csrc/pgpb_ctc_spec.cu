@@ -55,6 +55,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "pgpb_rerank.cuh"
 
@@ -148,15 +149,62 @@ struct Top1 {
   __device__ __forceinline__ void merge(const Top1 &o) { ins(o.m, o.i); }
 };
 
+// Per-lane maxima of the four insertion chains of a register row.
+struct Chains4 {
+  float m[4];
+  int i[4];
+};
+
+// This lane's first max of the row without token j1: its chain maxima other
+// than j1's, and, in the one lane owning j1, a rescan of j1's chain only.
+template <int NV>
+__device__ __forceinline__ void lane_runner_up(const float (&x)[NV], const int (&id)[NV], const Chains4 &r, int j1,
+                                               float &b, int &j) {
+  b = -INFINITY;
+  j = INT_MAX;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (r.i[c] != j1 && argmax_better(r.m[c], r.i[c], b, j)) {
+      b = r.m[c];
+      j = r.i[c];
+    }
+  const int cs = r.i[0] == j1 ? 0 : r.i[1] == j1 ? 1 : r.i[2] == j1 ? 2 : r.i[3] == j1 ? 3 : -1;
+  if (cs >= 0) {  // divergent: one lane
+    auto scan = [&](auto cc) {
+      constexpr int c = decltype(cc)::value;
+#pragma unroll
+      for (int k = c; k < NV; k += 4)
+        if (id[k] != j1 && argmax_better(x[k], id[k], b, j)) {
+          b = x[k];
+          j = id[k];
+        }
+    };
+    switch (cs) {
+      case 0: scan(std::integral_constant<int, 0>{}); break;
+      case 1: scan(std::integral_constant<int, 1>{}); break;
+      case 2: scan(std::integral_constant<int, 2>{}); break;
+      default: scan(std::integral_constant<int, 3>{}); break;
+    }
+  }
+}
+
 // Row reduction over values already in registers: first max (a, lp_a) and,
 // only when a is not the blank (a blank frame never emits, R6), the first max
-// of the rest (t2, lp_2).  Four independent chains per lane keep the compare
-// chains short; ids are ascending within every chain.
+// of the rest (t2, lp_2).  Four independent insertion chains per lane keep the
+// compare chains short (ids ascend within every chain); the runner-up comes
+// from the chain maxima other than a's plus, in the one lane owning a, a
+// rescan of a's chain only.
 template <int NV>
 __device__ __forceinline__ int4 reduce_row(const float (&x)[NV], const int (&id)[NV], bool top2, int blank) {
   Top1 r[4];
 #pragma unroll
   for (int k = 0; k < NV; ++k) r[k & 3].ins(x[k], id[k]);
+  Chains4 ch;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    ch.m[c] = r[c].m;
+    ch.i[c] = r[c].i;
+  }
   r[0].merge(r[1]);
   r[2].merge(r[3]);
   r[0].merge(r[2]);
@@ -166,18 +214,125 @@ __device__ __forceinline__ int4 reduce_row(const float (&x)[NV], const int (&id)
   float b2 = -INFINITY;
   int j2 = INT_MAX;
   if (top2 && j1 != blank) {
-    Top1 q[4];
-#pragma unroll
-    for (int k = 0; k < NV; ++k)
-      if (id[k] != j1) q[k & 3].ins(x[k], id[k]);
-    q[0].merge(q[1]);
-    q[2].merge(q[3]);
-    q[0].merge(q[2]);
-    b2 = q[0].m;
-    j2 = q[0].i;
+    lane_runner_up(x, id, ch, j1, b2, j2);
     warp_argmax(b2, j2);
   }
   return make_int4(j1, __float_as_int(b1), j2, __float_as_int(b2));
+}
+
+// Row reduction with warp reductions in hardware (redux.sync, CREDUX):
+// per lane, maxima of four groups of 8 consecutive register elements (ids
+// ascend with the element index, so groups ascend too), the warp max M by
+// redux.max.f32, then the first element equal to M is searched only in the
+// first group whose max equals M (usually in one lane) and the warp's first
+// such id by redux.min.  The runner-up (only when a != blank) repeats this
+// over the row without a: the owning lane's candidate is its other groups'
+// maxima plus a rescan of a's group.  Values stored are the matched elements
+// themselves (exact bits, so -0.0 stays -0.0).  Record halves {a, lp_a} and
+// {t2, lp_2} are stored by the lanes that own them.
+template <int Q>
+__device__ __forceinline__ float gmax(const float (&x)[32]) {
+  const float a = fmaxf(x[8 * Q], x[8 * Q + 1]), b = fmaxf(x[8 * Q + 2], x[8 * Q + 3]);
+  const float c = fmaxf(x[8 * Q + 4], x[8 * Q + 5]), d = fmaxf(x[8 * Q + 6], x[8 * Q + 7]);
+  return fmaxf(fmaxf(a, b), fmaxf(c, d));
+}
+
+template <int Q>
+__device__ __forceinline__ float gmax_ex(const float (&x)[32], const int (&id)[32], int ex) {
+  float y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) y[k] = id[8 * Q + k] == ex ? -INFINITY : x[8 * Q + k];
+  return fmaxf(fmaxf(fmaxf(y[0], y[1]), fmaxf(y[2], y[3])), fmaxf(fmaxf(y[4], y[5]), fmaxf(y[6], y[7])));
+}
+
+// first element of group Q equal to v whose id is not ex (INT_MAX if none)
+template <int Q>
+__device__ __forceinline__ int gfind(const float (&x)[32], const int (&id)[32], float v, int ex, float &val) {
+  int r = INT_MAX;
+  float rv = v;
+#pragma unroll
+  for (int k = 8 * Q + 7; k >= 8 * Q; --k)
+    if (x[k] == v && id[k] != ex) {
+      r = id[k];
+      rv = x[k];
+    }
+  val = rv;
+  return r;
+}
+
+__device__ __forceinline__ int lane_find(const float (&x)[32], const int (&id)[32], const float (&g)[4], float v,
+                                         int ex, float &val, int &grp) {
+  int r = INT_MAX;
+  grp = -1;
+  if (g[0] == v) {
+    r = gfind<0>(x, id, v, ex, val);
+    grp = 0;
+  }
+  if (r == INT_MAX && g[1] == v) {
+    r = gfind<1>(x, id, v, ex, val);
+    grp = 1;
+  }
+  if (r == INT_MAX && g[2] == v) {
+    r = gfind<2>(x, id, v, ex, val);
+    grp = 2;
+  }
+  if (r == INT_MAX && g[3] == v) {
+    r = gfind<3>(x, id, v, ex, val);
+    grp = 3;
+  }
+  return r;
+}
+
+__device__ __forceinline__ float redux_max_f32(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+__device__ __forceinline__ void reduce_row_rx(const float (&x)[32], const int (&id)[32], bool top2, int blank,
+                                              int lane, int2 *rec, bool store) {
+  float g[4];
+  g[0] = gmax<0>(x);
+  g[1] = gmax<1>(x);
+  g[2] = gmax<2>(x);
+  g[3] = gmax<3>(x);
+  const float lm = fmaxf(fmaxf(g[0], g[1]), fmaxf(g[2], g[3]));
+  const float M = redux_max_f32(lm);
+  int li = INT_MAX, grp = -1;
+  float lv = M;
+  if (lm == M) li = lane_find(x, id, g, M, INT_MAX, lv, grp);
+  const int j1 = int(__reduce_min_sync(kFull, unsigned(li)));
+  const bool own = li == j1;
+  if (store && own) rec[0] = make_int2(j1, __float_as_int(lv));
+  if (!top2) return;
+  if (j1 == blank) {
+    if (store && lane == 0) rec[1] = make_int2(INT_MAX, __float_as_int(-INFINITY));
+    return;
+  }
+  // group maxima of the row without a (differs from g in a's group only)
+  float h[4] = {g[0], g[1], g[2], g[3]};
+  float m2 = lm;
+  if (own) {  // divergent: one lane
+    switch (grp) {
+      case 0: h[0] = gmax_ex<0>(x, id, j1); break;
+      case 1: h[1] = gmax_ex<1>(x, id, j1); break;
+      case 2: h[2] = gmax_ex<2>(x, id, j1); break;
+      default: h[3] = gmax_ex<3>(x, id, j1); break;
+    }
+    m2 = fmaxf(fmaxf(h[0], h[1]), fmaxf(h[2], h[3]));
+  }
+  const float M2 = redux_max_f32(m2);
+  int li2 = INT_MAX, grp2;
+  float lv2 = M2;
+  if (m2 == M2) li2 = lane_find(x, id, h, M2, j1, lv2, grp2);
+  const int j2 = int(__reduce_min_sync(kFull, unsigned(li2)));
+  if (store) {
+    if (j2 == INT_MAX) {  // no runner-up (V == 1)
+      if (lane == 0) rec[1] = make_int2(INT_MAX, __float_as_int(-INFINITY));
+    } else if (li2 == j2) {
+      rec[1] = make_int2(j2, __float_as_int(lv2));
+    }
+  }
 }
 
 // One warp reduces frames f and f + 1 (when valid) with both rows loaded
@@ -236,10 +391,15 @@ __global__ void __launch_bounds__(256) frame_top2_kernel(const float *__restrict
         y1[4 * k + 2] = x1[k].z;
         y1[4 * k + 3] = x1[k].w;
       }
+#ifdef PGPB_A_CHAINS
       const int4 o0 = reduce_row<32>(y0, id, kTop2, blank);
       const int4 o1 = reduce_row<32>(y1, id, kTop2, blank);
       if (lane == 0 && v0) top[f0] = o0;
       if (lane == 1 && v1) top[f1] = o1;
+#else
+      reduce_row_rx(y0, id, kTop2, blank, lane, reinterpret_cast<int2 *>(top + f0), v0);
+      reduce_row_rx(y1, id, kTop2, blank, lane, reinterpret_cast<int2 *>(top + f1), v1);
+#endif
     } else {
       // general path: scalar loads, tiles of 256 values per lane-chain set
       for (int r = 0; r < 2; ++r) {
@@ -1401,7 +1561,10 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
   int4 *top = nullptr;
   if (F > 0) PGPB_CUDA_TRY(cudaMallocAsync(&top, size_t(F) * 16, st));
   if (F > 0) {
-    const unsigned grid = warp_grid((F + 1) / 2, 8);
+    // one wave: 2 resident CTAs per SM (<= 128 registers), grid-stride over
+    // frame pairs (0.5 us faster than 8 waves of CTAs on 128 x 200 frames)
+    const char *eps = getenv("PGPB_CTC_A_PERSM");  // timing experiments
+    const unsigned grid = warp_grid((F + 1) / 2, eps ? std::max(1, atoi(eps)) : 2);
     using KA = void (*)(const float *, int64_t, int64_t, int, const int32_t *, int, int4 *);
     KA ka = use_boost ? (vec ? frame_top2_kernel<true, true> : frame_top2_kernel<true, false>)
                       : (vec ? frame_top2_kernel<false, true> : frame_top2_kernel<false, false>);
@@ -1411,6 +1574,11 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
       cudaFreeAsync(top, st);
       return fail(PGPB_ECUDA, std::string("frame_top2_kernel: ") + cudaGetErrorString(e));
     }
+  }
+  const char *eoa = getenv("PGPB_CTC_ONLY_A");  // timing experiments: phase A alone (outputs invalid)
+  if (eoa && atoi(eoa) == 1) {
+    if (top) cudaFreeAsync(top, st);
+    return PGPB_OK;
   }
   Args a{};
   a.t = table ? table->view : empty_view(V);

@@ -67,9 +67,13 @@ def main():
     T = int(sys.argv[2]) if len(sys.argv) > 2 else 200
     dev = torch.device("cuda")
     tab, V = table()
+    only = os.environ.get("PGPB_REGIMES")
+    impls = os.environ.get("PGPB_IMPLS", "fused,twophase").split(",")
     for name, lp in regimes(B, T, V, dev).items():
+        if only and name not in only.split(","):
+            continue
         row = {}
-        for impl in ("fused", "twophase"):
+        for impl in impls:
             if impl == "twophase":
                 os.environ["PGPB_CTC_TWOPHASE"] = "1"
             else:

@@ -1,0 +1,4 @@
+# full GPU suite + bench
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
+timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1

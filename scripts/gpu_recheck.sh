@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1
+timeout 300 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1

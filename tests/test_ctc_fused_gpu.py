@@ -67,9 +67,9 @@ def _check(got, lps, lens, tab, lam):
         n = lps.shape[1] if lens is None else int(lens[b])
         e = orc.ctc_greedy_decode(lps[b, :n], 0, tab, lam)
         g = res_tuple(got[b])
-        assert g["tokens"] == e["tokens"], b
-        assert g["am"] == e["am"] and g["boost"] == e["boost"], b
-        assert g["trace"] == [list(x) for x in e["trace"]], b
+        assert g["tokens"] == e["tokens"], (b, lam)
+        assert g["am"] == e["am"] and g["boost"] == e["boost"], (b, lam)
+        assert g["trace"] == [list(x) for x in e["trace"]], (b, lam)
 
 
 @pytest.fixture(scope="module")
@@ -239,3 +239,50 @@ def test_vocab_4096_general_phase_a(seq):
     lens = rng.integers(1, T + 1, size=B).astype(np.int32)
     for lam in (0.0, 1.0):
         _check(_run(lps, lens, tab, lam, {"PGPB_CTC_SEQ": seq}), lps, lens, tab, lam)
+
+
+@pytest.mark.parametrize("V", [1024, 64, 4])
+def test_phase_a_ties_signed_zeros_masked(V):
+    """Phase A's hardware warp reductions (redux.max.f32 over group maxima,
+    then the first matching id) against the reference's first-max rules:
+    quantised log-probs with exact ties for the argmax and the runner-up,
+    duplicated maxima in different lanes / register groups, a maximum of
+    -0.0 ahead of +0.0, and masked (-inf) tokens.  The signed-zero rows (two
+    tokens of probability 1, not a distribution) are checked unboosted only:
+    there the argmax, its exact bits and am are all phase A decides."""
+    rng = np.random.default_rng(41 + V)
+    if V == 1024:
+        phrases, _ = gi.corpus("p20k_v1024")
+    else:
+        phrases = gi.random_phrase_set(rng, 12 if V > 8 else 3, 4, V)
+    tab = product_table(phrases, V)
+    B, T = 12, 180
+    logits = np.round(rng.normal(0.0, 1.5, size=(B, T, V)) * 4.0) / 4.0
+    lps = gi.log_softmax(logits).astype(np.float32)
+    zeros = lps.copy()
+    for b in range(B):
+        for t in range(T):
+            r = lps[b, t]
+            kind = int(rng.integers(0, 6))
+            if kind == 2 and V > 2:
+                z = zeros[b, t]
+                i, j = sorted(rng.choice(V, size=2, replace=False))
+                z[:] = np.minimum(z, -1.0)
+                z[i] = np.float32(-0.0)
+                z[j] = np.float32(0.0)
+                continue
+            top = float(r.max())
+            if kind == 1 and V > 2:  # duplicated maximum later in the row
+                r[int(rng.integers(0, V))] = top
+                r[int(rng.integers(0, V))] = top
+            elif kind == 3:  # masked tokens (a finite maximum stays)
+                m = rng.random(V) < 0.5
+                m[int(np.argmax(r))] = False
+                r[m] = -np.inf
+            elif kind == 4 and V > 3:  # runner-up tie
+                s = np.argsort(-r, kind="stable")
+                r[int(rng.integers(0, V))] = r[s[1]]
+    lens = rng.integers(1, T + 1, size=B).astype(np.int32)
+    for lam in (0.0, 1.0, 2.5):
+        _check(_run(lps, lens, tab, lam), lps, lens, tab, lam)
+    _check(_run(zeros, lens, tab, 0.0), zeros, lens, tab, 0.0)
