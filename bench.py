@@ -276,6 +276,9 @@ def run_ours(args, rank, world, local):
         "gpu_launches": args.steps + e2e_steps,
         "clocks": clk.summary(),
     }
+    if world == 1:
+        out["advance_sweep"] = bench_advance_sweep(dtab, S, V, dev, hbm_peak)
+        out["gpu_launches"] += out["advance_sweep"].pop("_launches", 0)
     if not args.no_decode:
         out["decode_rnnt"] = bench_rnnt(tab, V, dev, rank, world)
         out["gpu_launches"] += out["decode_rnnt"].pop("_launches", 0)
@@ -368,6 +371,59 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
         del lp
     out["_launches"] = launches
     return out
+
+
+def bench_advance_sweep(dtab, S, V, dev, hbm_peak, batches=(128, 1024, 8192, 65536), steps=20):
+    """SURVEY 8(d) batch sweep of the advance on one GPU: K back-to-back
+    launches in one graph over an output ring larger than L2 (>= 256 MiB),
+    uniform random states; device time per launch and the fraction of the
+    measured HBM peak (8 B per cell + 4 B per state)."""
+    import torch
+
+    from paper_2508_07014_b200 import _lib
+
+    rng = np.random.default_rng(77)
+    res = {"note": "graph of %d launches per batch, outputs rotate over >= 256 MiB" % steps, "_launches": 0}
+    for B in batches:
+        per = B * V * 8
+        ring = max(2, min(steps, -(-256 * 2**20 // per)))
+        states = torch.from_numpy(rng.integers(0, S, size=(steps, B)).astype(np.int32)).to(dev)
+        outs = [(torch.empty((B, V), dtype=torch.float32, device=dev), torch.empty((B, V), dtype=torch.int32, device=dev))
+                for _ in range(ring)]
+
+        def step(i):
+            sc, nx = outs[i % ring]
+            _lib.check(_lib.LIB.pgpb_advance(dtab.handle, states[i].data_ptr(), B, sc.data_ptr(), nx.data_ptr(),
+                                             _lib.stream_ptr()))
+
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for i in range(3):
+                step(i)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(steps):
+                step(i)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = None
+        for _ in range(3):
+            a.record()
+            g.replay()
+            b.record()
+            torch.cuda.synchronize(dev)
+            ms = a.elapsed_time(b) / steps
+            best = ms if best is None else min(best, ms)
+        gbs = (B * V * 8 + B * 4) / (best / 1e3) / 1e9
+        res[str(B)] = {"ms_per_launch": best, "cells_per_s": B * V / (best / 1e3), "GBps": gbs,
+                       "frac_hbm": gbs / hbm_peak}
+        res["_launches"] += 3 + 4 * steps
+        del outs, states, g
+        torch.cuda.empty_cache()
+    return res
 
 
 def cpu_ctc_reference(lps, tab, B, T, budget_s=2.0):
