@@ -329,6 +329,16 @@ def _ctc_regimes(B, T, V, dev, rank):
     del lp
     logits[:, torch.arange(T, device=dev) % 4 != 0, 0] += 10.0
     yield "blank3", torch.log_softmax(logits, dim=-1)
+    del logits
+    # the clean shape at 5x the utterance length (40 s): the walker's latency
+    # is per utterance, phase A's bandwidth cost per frame
+    TL = 5 * T
+    ems = []
+    for _ in range(B):
+        tgt = [int(x) for x in rng.integers(1, V, size=TL // 4 + 1)]
+        ems.append(synth_ctc_emissions(tgt, vocab, margin=0.5, seed=int(rng.integers(2**31)), boost_positions=[],
+                                       blanks_between=3).logprobs[:TL])
+    yield f"clean_T{TL}", torch.from_numpy(np.stack(ems)).to(dev)
 
 
 def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
@@ -360,8 +370,9 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
             torch.cuda.synchronize(dev)
             launches += 2 * reps
             ms = s.elapsed_time(e) / reps
-            res[name] = {"ms": ms, "rtfx": B * T * FRAME_SEC / (ms / 1e3) * world,
-                         "hbm_gbs": B * T * V * 4 / (ms / 1e3) / 1e9}
+            Tr = lp.shape[1]
+            res[name] = {"ms": ms, "rtfx": B * Tr * FRAME_SEC / (ms / 1e3) * world,
+                         "hbm_gbs": B * Tr * V * 4 / (ms / 1e3) / 1e9}
             if name == "boosted":
                 res["emitted_per_utt"] = float(o.num_out.double().mean().item())
         res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
