@@ -243,6 +243,31 @@ int pgpb_label_loop_step(const pgpb_table *table, const float *d_logprobs, int64
                          int32_t use_boost, const pgpb_label_loop_state *state,
                          uint8_t *d_emit, int64_t *d_feed, int32_t *d_any_active, void *stream);
 
+/* pgpb_label_loop_step with the joint's log-softmax fused in: row r's bf16
+ * logits (row stride ld_logits) are log-softmaxed in fp32 into lp_out[r]
+ * (stride vocab_size; torch's formula order (x - max) - log(sum exp(x -
+ * max))), which the decision then reads; lp_out doubles as the record of
+ * the log-probs each row was decided on.  Config-2 decoder glue
+ * (rnnt.py), same decision and bookkeeping as pgpb_label_loop_step.      */
+int pgpb_label_loop_step_logits(const pgpb_table *table, const void *d_logits_bf16, int64_t ld_logits,
+                                float *d_lp_out, int64_t rows, int32_t vocab_size, int32_t blank,
+                                double lam, int32_t use_boost, const pgpb_label_loop_state *state,
+                                uint8_t *d_emit, int64_t *d_feed, int32_t *d_any_active, void *stream);
+
+/* Config-2 prediction / joint network glue (rnnt.py; no reference
+ * counterpart: the reference's transducer decoders take a host StepModel,
+ * acoustic.py:203-255).  bf16 tensors, row-major.
+ *  joint_hidden: z[b, :J] = relu(enc_proj[b, min(t[b], max(len[b]-1, 0)), :J]
+ *                + pred_proj[b, :J]); enc_proj row stride per utterance ld_b.
+ *  lstm_update:  gates = E[feed[b]] + hg[b] (E[V, 4H] = emb W_ih^T + b_ih,
+ *                hg[B, 4H] = h W_hh^T + b_hh; gate order i, f, g, o), LSTM
+ *                cell in fp32, h[b], c[b] overwritten iff emit[b] (NULL: all). */
+int pgpb_rnnt_joint_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, const int64_t *d_t,
+                           const int64_t *d_lengths, const void *d_pred_proj, void *d_z, int64_t B,
+                           void *stream);
+int pgpb_rnnt_lstm_update(const void *d_E, const int64_t *d_feed, const void *d_hg, const uint8_t *d_emit,
+                          void *d_h, void *d_c, int64_t B, int32_t H, void *stream);
+
 /* Per-state maximum of the resolved score row, max_v scores[s, v]
  * (used by the AED eos bump, decoding.py:546-552).  out[S] f32.             */
 int pgpb_row_max(const pgpb_table *table, float *d_out, void *stream);

@@ -103,6 +103,10 @@ _SIGS = {
     "pgpb_row_max": [c_void_p, _P, c_void_p],
     "pgpb_label_loop_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32,
                              POINTER(LabelLoopState), _P, _P, _P, c_void_p],
+    "pgpb_label_loop_step_logits": [c_void_p, _P, c_int64, _P, c_int64, c_int32, c_int32, c_double, c_int32,
+                                    POINTER(LabelLoopState), _P, _P, _P, c_void_p],
+    "pgpb_rnnt_joint_hidden": [_P, c_int64, c_int32, _P, _P, _P, _P, c_int64, c_void_p],
+    "pgpb_rnnt_lstm_update": [_P, _P, _P, _P, _P, _P, c_int64, c_int32, c_void_p],
     "pgpb_beam_topk": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_int32, _P, _P, _P, _P,
                        _P, _P, _P, c_double, c_int32, c_int32, _P, _P, _P, _P, _P, _P, c_void_p],
     "pgpb_tbeam_wave": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32, c_int32,

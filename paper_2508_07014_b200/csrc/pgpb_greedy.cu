@@ -12,6 +12,8 @@
 
 #include <string>
 
+#include <cuda_bf16.h>
+
 #include "pgpb_rerank.cuh"
 
 namespace pgpb {
@@ -30,6 +32,30 @@ struct RowDecision {
   int next;
   bool blank;
 };
+
+// decide_row with the state's blob already loaded (issued before the row's
+// own work, so its dependent round trips overlap the top-M pass).
+template <int NC>
+__device__ __forceinline__ RowDecision decide_row_pre(const TableView &t, const float *row, int V, int blank,
+                                                      double lam, int use_boost, const BlobRegs &cur, unsigned *bm,
+                                                      float *sv, int *si, int lane) {
+  int tv[kStepTopM];
+  float tx[kStepTopM];
+  if (NC > 0)
+    warp_row_topm_thr<kStepTopM, (NC > 0 ? NC : 1)>(row, V, lane, sv, si, tv, tx);
+  else
+    warp_row_topm<kStepTopM, false>(row, V, lane, tv, tx);
+  RowDecision d{tv[0], tx[0], 0.0, 0, tv[0] == blank};
+  if (!d.blank && use_boost) {
+    const BCand w = blob_rerank_regs<kStepTopM>(t, cur, t.root_scores, t.root_next, t.root_next_off, bm, row, V, tv,
+                                                tx, blank, -1, lam, t.max_root_score, lane);
+    d.chosen = w.v;
+    d.lp = w.lp;
+    d.delta = static_cast<double>(w.s);
+    d.next = w.nx;
+  }
+  return d;
+}
 
 template <int NC>
 __device__ __forceinline__ RowDecision decide_row(const TableView &t, const float *row, int V, int blank, double lam,
@@ -97,11 +123,29 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Row log-softmax of bf16 logits into f32 (torch's formula order:
+// (x - max) - log(sum exp(x - max)), accurate expf / logf), one warp.
+__device__ __forceinline__ void warp_log_softmax_bf16(const __nv_bfloat16 *__restrict__ x, float *__restrict__ y,
+                                                      int V, int lane) {
+  float m = -INFINITY;
+  for (int v = lane; v < V; v += 32) m = fmaxf(m, __bfloat162float(x[v]));
+  float mr;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(m));
+  float s = 0.0f;
+  for (int v = lane; v < V; v += 32) s += expf(__bfloat162float(x[v]) - mr);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  const float ls = logf(s);
+  for (int v = lane; v < V; v += 32) y[v] = (__bfloat162float(x[v]) - mr) - ls;
+  __syncwarp();  // the row is read back by the whole warp (memory ordering)
+}
+
 template <int NC>
 __global__ void __launch_bounds__(kThreads)
-    label_loop_kernel(TableView t, int use_boost, const float *__restrict__ lp, int64_t ld, int64_t R, int V,
+    label_loop_kernel(TableView t, int use_boost, const float *lp, int64_t ld, int64_t R, int V,
                       int blank, double lam, pgpb_label_loop_state st, uint8_t *__restrict__ emit,
-                      int64_t *__restrict__ feed, int32_t *__restrict__ any_active) {
+                      int64_t *__restrict__ feed, int32_t *__restrict__ any_active,
+                      const __nv_bfloat16 *__restrict__ logits, int64_t ld_logits) {
   extern __shared__ __align__(16) unsigned char smem[];
   const StepScratch sc = step_scratch(smem, V, use_boost);
   const int lane = threadIdx.x & 31;
@@ -115,8 +159,15 @@ __global__ void __launch_bounds__(kThreads)
       }
       continue;
     }
-    const RowDecision d = decide_row<NC>(t, lp + r * ld, V, blank, lam, use_boost, use_boost ? st.tree[r] : 0,
-                                         sc.bm, sc.sv, sc.si, lane);
+    // the tree state's blob first: its two dependent round trips overlap
+    // the row's log-softmax and top-M pass
+    BlobRegs cur{};
+    if (use_boost) cur = load_blob(t, __ldg(t.blob_off + st.tree[r]), lane);
+    // fused joint tail: log-softmax of the row's logits, written out (the
+    // row the decision reads, and the record of what was decided on)
+    if (logits) warp_log_softmax_bf16(logits + r * ld_logits, const_cast<float *>(lp) + r * ld, V, lane);
+    const RowDecision d = decide_row_pre<NC>(t, lp + r * ld, V, blank, lam, use_boost, cur, sc.bm, sc.sv, sc.si,
+                                             lane);
     if (lane == 0) {
       // R7 bookkeeping (decoding.py:371-392)
       st.am[r] = st.am[r] + static_cast<double>(d.lp);
@@ -160,7 +211,7 @@ __global__ void __launch_bounds__(kThreads)
 using StepFn = void (*)(TableView, int, const float *, int64_t, int64_t, int, const int32_t *, const uint8_t *, int,
                         double, int32_t *, float *, double *, int32_t *, uint8_t *);
 using LoopFn = void (*)(TableView, int, const float *, int64_t, int64_t, int, int, double, pgpb_label_loop_state,
-                        uint8_t *, int64_t *, int32_t *);
+                        uint8_t *, int64_t *, int32_t *, const __nv_bfloat16 *, int64_t);
 
 // NC = float4 chunks per lane for the register top-M (V <= 1024, 16-byte
 // rows); 0 selects the generic path.
@@ -243,9 +294,33 @@ int pgpb_greedy_step(const pgpb_table *table, const float *d_lp, int64_t ld, int
   return PGPB_OK;
 }
 
+static int label_loop_launch(const pgpb_table *table, const float *d_lp, int64_t ld, int64_t R, int32_t V,
+                             int32_t blank, double lam, int32_t use_boost, const pgpb_label_loop_state *state,
+                             uint8_t *d_emit, int64_t *d_feed, int32_t *d_any_active, const void *d_logits,
+                             int64_t ld_logits, void *stream);
+
 int pgpb_label_loop_step(const pgpb_table *table, const float *d_lp, int64_t ld, int64_t R, int32_t V, int32_t blank,
                          double lam, int32_t use_boost, const pgpb_label_loop_state *state, uint8_t *d_emit,
                          int64_t *d_feed, int32_t *d_any_active, void *stream) {
+  return label_loop_launch(table, d_lp, ld, R, V, blank, lam, use_boost, state, d_emit, d_feed, d_any_active,
+                           nullptr, 0, stream);
+}
+
+int pgpb_label_loop_step_logits(const pgpb_table *table, const void *d_logits_bf16, int64_t ld_logits,
+                                float *d_lp_out, int64_t R, int32_t V, int32_t blank, double lam, int32_t use_boost,
+                                const pgpb_label_loop_state *state, uint8_t *d_emit, int64_t *d_feed,
+                                int32_t *d_any_active, void *stream) {
+  using namespace pgpb;
+  if (!d_logits_bf16 || !d_lp_out) return fail(PGPB_EINVAL, "NULL buffer");
+  if (ld_logits < V) return fail(PGPB_EINVAL, "bad shape");
+  return label_loop_launch(table, d_lp_out, V, R, V, blank, lam, use_boost, state, d_emit, d_feed, d_any_active,
+                           d_logits_bf16, ld_logits, stream);
+}
+
+static int label_loop_launch(const pgpb_table *table, const float *d_lp, int64_t ld, int64_t R, int32_t V,
+                             int32_t blank, double lam, int32_t use_boost, const pgpb_label_loop_state *state,
+                             uint8_t *d_emit, int64_t *d_feed, int32_t *d_any_active, const void *d_logits,
+                             int64_t ld_logits, void *stream) {
   using namespace pgpb;
   if (R < 0 || V < 1 || ld < V || !state) return fail(PGPB_EINVAL, "bad shape");
   if (state->cap < 1) return fail(PGPB_EINVAL, "cap must be >= 1");
@@ -261,8 +336,9 @@ int pgpb_label_loop_step(const pgpb_table *table, const float *d_lp, int64_t ld,
   int rc = prep_kernel(fn, smem);
   if (rc) return rc;
   const unsigned grid = static_cast<unsigned>((R + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  fn<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(t, use_boost ? 1 : 0, d_lp, ld, R, V, blank, lam,
-                                                                  *state, d_emit, d_feed, d_any_active);
+  fn<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      t, use_boost ? 1 : 0, d_lp, ld, R, V, blank, lam, *state, d_emit, d_feed, d_any_active,
+      static_cast<const __nv_bfloat16 *>(d_logits), ld_logits);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }

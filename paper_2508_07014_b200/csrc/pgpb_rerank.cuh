@@ -52,7 +52,7 @@ __device__ RerankOut warp_rerank(const TableView &t, const float *root, const in
   if (kVec) {
     const float4 *row4 = reinterpret_cast<const float4 *>(row);
     for (int i = lane; i < (V >> 2); i += 32) {
-      const float4 x4 = __ldg(row4 + i);
+      const float4 x4 = __ldcg(row4 + i);
       const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -66,14 +66,14 @@ __device__ RerankOut warp_rerank(const TableView &t, const float *root, const in
     for (int v = lane; v < V; v += 32) {
       if (v == ex1 || v == ex2) continue;
       if ((bm[v >> 5] >> (v & 31)) & 1u) continue;
-      consider(v, __ldg(row + v), acc + root[v], rnext[v]);
+      consider(v, __ldcg(row + v), acc + root[v], rnext[v]);
     }
   }
   // Explicit first-hit arcs of the chain.
   for (int i = lane; i < rec.y; i += 32) {
     const int4 e = __ldg(t.clo + rec.x + i);
     if (e.x == ex1 || e.x == ex2) continue;
-    consider(e.x, __ldg(row + e.x), __int_as_float(e.z), e.y);
+    consider(e.x, __ldcg(row + e.x), __int_as_float(e.z), e.y);
   }
   // Warp reduction on (c, lp, v); the winning lane then broadcasts (s, next).
   double rc = bc;
@@ -113,7 +113,7 @@ __device__ __forceinline__ void warp_row_argmax(const float *__restrict__ row, i
     const float4 *row4 = reinterpret_cast<const float4 *>(row);
 #pragma unroll 4
     for (int i = lane; i < (V >> 2); i += 32) {
-      const float4 x = __ldg(row4 + i);
+      const float4 x = __ldcg(row4 + i);
       const int v = 4 * i;
       if (argmax_better(x.x, v, best, idx)) { best = x.x; idx = v; }
       if (argmax_better(x.y, v + 1, best, idx)) { best = x.y; idx = v + 1; }
@@ -122,7 +122,7 @@ __device__ __forceinline__ void warp_row_argmax(const float *__restrict__ row, i
     }
   } else {
     for (int v = lane; v < V; v += 32) {
-      const float x = __ldg(row + v);
+      const float x = __ldcg(row + v);
       if (argmax_better(x, v, best, idx)) { best = x; idx = v; }
     }
   }
@@ -426,14 +426,14 @@ __device__ __forceinline__ void warp_row_topm(const float *__restrict__ row, int
     const float4 *row4 = reinterpret_cast<const float4 *>(row);
 #pragma unroll 4
     for (int c = lane; c < (V >> 2); c += 32) {
-      const float4 x = __ldg(row4 + c);
+      const float4 x = __ldcg(row4 + c);
       topm_insert<M>(lv, li, x.x, 4 * c);
       topm_insert<M>(lv, li, x.y, 4 * c + 1);
       topm_insert<M>(lv, li, x.z, 4 * c + 2);
       topm_insert<M>(lv, li, x.w, 4 * c + 3);
     }
   } else {
-    for (int v = lane; v < V; v += 32) topm_insert<M>(lv, li, __ldg(row + v), v);
+    for (int v = lane; v < V; v += 32) topm_insert<M>(lv, li, __ldcg(row + v), v);
   }
 #pragma unroll
   for (int r = 0; r < M; ++r) {
@@ -473,7 +473,7 @@ __device__ __forceinline__ void warp_row_topm_thr(const float *__restrict__ row,
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
     const int c = lane + 32 * k;
-    x[k] = c < V4 ? __ldg(row4 + c) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    x[k] = c < V4 ? __ldcg(row4 + c) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
   }
   float lm = -INFINITY;
   int li = INT_MAX;

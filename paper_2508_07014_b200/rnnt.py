@@ -93,6 +93,9 @@ class RNNTModel:
                 raise ValueError("durations must be >= 0")
             self.w_dur = w(len(self.durations), J, fan_in=J) * 3.0
             self.dur_values = torch.tensor(self.durations, device=device, dtype=torch.int32)
+        # input gates of every token, emb @ W_ih^T + b_ih (one GEMM per model):
+        # a prediction step then gathers its row instead of embedding + GEMM
+        self.E = torch.addmm(self.b_lstm, self.emb, self.w_ih.T) if dt == torch.bfloat16 else None
 
     def project_encoder(self, enc):
         """enc [B,T,D] -> [B,T,J] (computed once per batch)."""
@@ -142,7 +145,7 @@ class LabelLoopingDecoder:
     """
 
     def __init__(self, model: RNNTModel, table: ArcTable | None, cfg: DecodeConfig, batch: int, max_frames: int,
-                 *, use_graph: bool = True, poll: int = 16, device=None):
+                 *, use_graph: bool = True, poll: int = 16, device=None, fused: bool = True):
         torch = _torch()
         self.torch = torch
         self.model, self.table, self.cfg = model, table, cfg
@@ -180,6 +183,9 @@ class LabelLoopingDecoder:
         self.any_active = torch.zeros(1, device=d, dtype=i32)
         self.flag_host = torch.zeros(1, dtype=i32, pin_memory=True)
         self.rows = torch.arange(B, device=d)
+        # fused kernels for RNN-T (bf16 networks); TDT keeps the framework path
+        self.fused = fused and model.durations is None and model.E is not None
+        self.z = torch.zeros((B, model.J), device=d, dtype=model.dtype)
         self.graph = None
         p = lambda x: x.data_ptr()  # noqa: E731
         self.state = _lib.LabelLoopState(p(self.t), p(self.k), p(self.lengths), p(self.n), p(self.last), p(self.tree),
@@ -188,6 +194,8 @@ class LabelLoopingDecoder:
 
     # -- one label iteration (fixed kernel sequence) ------------------------
     def _iteration(self):
+        if self.fused:
+            return self._iteration_fused()
         torch, m = self.torch, self.model
         self.any_active.zero_()
         tf = torch.minimum(self.t, (self.lengths - 1).clamp(min=0))
@@ -206,6 +214,28 @@ class LabelLoopingDecoder:
         self.h.copy_(torch.where(e2, h2, self.h))
         self.c.copy_(torch.where(e2, c2, self.c))
 
+    def _iteration_fused(self):
+        """The same iteration as 3 bf16 GEMMs + 3 kernels: joint hidden (frame
+        gather + add + ReLU), log-softmax fused into the boosted step
+        (pgpb_label_loop_step_logits, which writes self.lp), and the LSTM cell
+        on the precomputed input gates, updating h, c of emitting rows."""
+        torch, m = self.torch, self.model
+        self.any_active.zero_()
+        pp = torch.addmm(m.b_joint, self.h, m.w_pred.T)
+        _lib.check(_lib.LIB.pgpb_rnnt_joint_hidden(
+            self.enc_proj.data_ptr(), self.T * m.J, m.J, self.t.data_ptr(), self.lengths.data_ptr(), pp.data_ptr(),
+            self.z.data_ptr(), self.B, _lib.stream_ptr()), "pgpb_rnnt_joint_hidden")
+        logits = torch.addmm(m.b_out, self.z, m.w_out.T)
+        _lib.check(_lib.LIB.pgpb_label_loop_step_logits(
+            self.handle, logits.data_ptr(), self.V, self.lp.data_ptr(), self.B, self.V, int(m.blank_id),
+            float(self.cfg.lam), int(self.use), _lib.ctypes.byref(self.state), self.emit.data_ptr(),
+            self.feed.data_ptr(), self.any_active.data_ptr(), _lib.stream_ptr(),
+        ), "pgpb_label_loop_step_logits")
+        hg = torch.addmm(m.b_hh, self.h, m.w_hh.T)
+        _lib.check(_lib.LIB.pgpb_rnnt_lstm_update(
+            m.E.data_ptr(), self.feed.data_ptr(), hg.data_ptr(), self.emit.data_ptr(), self.h.data_ptr(),
+            self.c.data_ptr(), self.B, m.H, _lib.stream_ptr()), "pgpb_rnnt_lstm_update")
+
     def _reset(self, enc_proj, lengths):
         torch = self.torch
         B, T = enc_proj.shape[0], enc_proj.shape[1]
@@ -219,6 +249,13 @@ class LabelLoopingDecoder:
             x.zero_()
         self.last.fill_(self.model.blank_id)
         # initial prediction state: one step on the start symbol (blank)
+        if self.fused:
+            m = self.model
+            hg = torch.addmm(m.b_hh, self.h, m.w_hh.T)
+            _lib.check(_lib.LIB.pgpb_rnnt_lstm_update(
+                m.E.data_ptr(), self.last.data_ptr(), hg.data_ptr(), None, self.h.data_ptr(), self.c.data_ptr(),
+                self.B, m.H, _lib.stream_ptr()), "pgpb_rnnt_lstm_update")
+            return
         h2, c2 = self.model.lstm_step(self.last, self.h, self.c)
         self.h.copy_(h2)
         self.c.copy_(c2)

@@ -41,8 +41,12 @@ def _replay_check(o, B, lengths, tab, lam, cap, blank=0):
             [list(x) for x in e["trace"]]
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("lam,cap", [(1.0, 5), (2.0, 2), (0.0, 3)])
-def test_label_looping_matches_reference_by_replay(lam, cap):
+def test_label_looping_matches_reference_by_replay(lam, cap, fused):
+    """Fused iteration (joint hidden + log-softmax fused into the boosted
+    step + LSTM cell kernels) and the framework iteration: every row's
+    decisions replayed into the oracle from the log-probs it was decided on."""
     import torch
 
     from paper_2508_07014_b200 import DecodeConfig
@@ -56,10 +60,18 @@ def test_label_looping_matches_reference_by_replay(lam, cap):
     g.manual_seed(7)
     enc = torch.randn((B, T, 64), generator=g, device="cuda")
     lengths = np.random.default_rng(1).integers(1, T + 1, size=B)
-    dec = LabelLoopingDecoder(model, tab, DecodeConfig(lam=lam, max_symbols_per_frame=cap), B, T, use_graph=False)
+    dec = LabelLoopingDecoder(model, tab, DecodeConfig(lam=lam, max_symbols_per_frame=cap), B, T, use_graph=False,
+                              fused=fused)
+    assert dec.fused == fused
     o = dec.decode(model.project_encoder(enc), torch.from_numpy(lengths), record=True)
     assert int(o.num_out.sum()) > 0
     _replay_check(o, B, lengths, tab, lam, cap)
+    if fused:
+        # the fused log-softmax matches torch's on the recorded rows' logits
+        # up to fp32 rounding (each recorded row is normalised)
+        lp = np.concatenate([r[0][r[1].astype(bool)] for r in o.records])
+        s = np.log(np.exp(lp.astype(np.float64)).sum(-1))
+        assert np.abs(s).max() < 1e-5
 
 
 def test_graph_replay_equals_eager_and_boost_changes_output():
