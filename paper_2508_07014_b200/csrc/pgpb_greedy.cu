@@ -127,6 +127,49 @@ __global__ void __launch_bounds__(kThreads)
 // (x - max) - log(sum exp(x - max)), accurate expf / logf), one warp.
 __device__ __forceinline__ void warp_log_softmax_bf16(const __nv_bfloat16 *__restrict__ x, float *__restrict__ y,
                                                       int V, int lane) {
+  if (V <= 1024 && (V & 7) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+    // register path: 8 bf16 per 16-byte load, the row read once
+    const int V8 = V >> 3;
+    float v[32];
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = lane + 32 * k;
+      uint4 q = make_uint4(0u, 0u, 0u, 0u);
+      if (c < V8) q = __ldg(reinterpret_cast<const uint4 *>(x) + c);
+      const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&q);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h2[i]);
+        v[8 * k + 2 * i] = c < V8 ? f.x : -INFINITY;
+        v[8 * k + 2 * i + 1] = c < V8 ? f.y : -INFINITY;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) m = fmaxf(m, v[i]);
+    float mr;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(m));
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s += expf(v[i] - mr);  // padding: expf(-inf) = 0
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    const float ls = logf(s);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = lane + 32 * k;
+      if (c < V8) {
+        float4 *o4 = reinterpret_cast<float4 *>(y + 8 * c);
+        o4[0] = make_float4((v[8 * k] - mr) - ls, (v[8 * k + 1] - mr) - ls, (v[8 * k + 2] - mr) - ls,
+                            (v[8 * k + 3] - mr) - ls);
+        o4[1] = make_float4((v[8 * k + 4] - mr) - ls, (v[8 * k + 5] - mr) - ls, (v[8 * k + 6] - mr) - ls,
+                            (v[8 * k + 7] - mr) - ls);
+      }
+    }
+    __syncwarp();
+    return;
+  }
   float m = -INFINITY;
   for (int v = lane; v < V; v += 32) m = fmaxf(m, __bfloat162float(x[v]));
   float mr;

@@ -34,6 +34,26 @@ __global__ void __launch_bounds__(256)
   const __nv_bfloat16 *e = enc + b * ld_b + tf * J;
   const __nv_bfloat16 *p = pp + b * J;
   __nv_bfloat16 *o = z + b * J;
+  if ((J & 7) == 0 && ((reinterpret_cast<uintptr_t>(e) | reinterpret_cast<uintptr_t>(p) |
+                        reinterpret_cast<uintptr_t>(o)) & 15) == 0) {
+    // 8 bf16 per 16-byte access
+    for (int j = threadIdx.x; j < (J >> 3); j += blockDim.x) {
+      const uint4 qe = reinterpret_cast<const uint4 *>(e)[j], qp = reinterpret_cast<const uint4 *>(p)[j];
+      const __nv_bfloat162 *he = reinterpret_cast<const __nv_bfloat162 *>(&qe);
+      const __nv_bfloat162 *hp = reinterpret_cast<const __nv_bfloat162 *>(&qp);
+      uint4 qo;
+      __nv_bfloat162 *ho = reinterpret_cast<__nv_bfloat162 *>(&qo);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 a = __bfloat1622float2(he[i]), c = __bfloat1622float2(hp[i]);
+        const __nv_bfloat162 sum = __floats2bfloat162_rn(a.x + c.x, a.y + c.y);
+        const float2 r = __bfloat1622float2(sum);
+        ho[i] = __floats2bfloat162_rn(r.x > 0.0f ? r.x : 0.0f, r.y > 0.0f ? r.y : 0.0f);
+      }
+      reinterpret_cast<uint4 *>(o)[j] = qo;
+    }
+    return;
+  }
   for (int j = threadIdx.x; j < J; j += blockDim.x) {
     const __nv_bfloat16 s = __float2bfloat16_rn(__bfloat162float(e[j]) + __bfloat162float(p[j]));
     o[j] = __hgt(s, __float2bfloat16_rn(0.0f)) ? s : __float2bfloat16_rn(0.0f);
@@ -50,6 +70,28 @@ __global__ void __launch_bounds__(256)
   if (emit && !emit[b]) return;
   const __nv_bfloat16 *ex = E + feed[b] * int64_t(4 * H);
   const __nv_bfloat16 *hx = hg + b * int64_t(4 * H);
+  if ((H & 1) == 0) {
+    // two hidden units per thread (bf16x2 accesses)
+    const __nv_bfloat162 *e2 = reinterpret_cast<const __nv_bfloat162 *>(ex);
+    const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(hx);
+    __nv_bfloat162 *c2 = reinterpret_cast<__nv_bfloat162 *>(c + b * H);
+    __nv_bfloat162 *h2 = reinterpret_cast<__nv_bfloat162 *>(h + b * H);
+    const int H2 = H >> 1;
+    for (int j = threadIdx.x; j < H2; j += blockDim.x) {
+      float2 g[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 a = __bfloat1622float2(e2[q * H2 + j]), d = __bfloat1622float2(x2[q * H2 + j]);
+        g[q] = make_float2(a.x + d.x, a.y + d.y);
+      }
+      const float2 cp = __bfloat1622float2(c2[j]);
+      const float cx = sigm(g[1].x) * cp.x + sigm(g[0].x) * tanhf(g[2].x);
+      const float cy = sigm(g[1].y) * cp.y + sigm(g[0].y) * tanhf(g[2].y);
+      c2[j] = __floats2bfloat162_rn(cx, cy);
+      h2[j] = __floats2bfloat162_rn(sigm(g[3].x) * tanhf(cx), sigm(g[3].y) * tanhf(cy));
+    }
+    return;
+  }
   for (int j = threadIdx.x; j < H; j += blockDim.x) {
     const float gi = __bfloat162float(ex[j]) + __bfloat162float(hx[j]);
     const float gf = __bfloat162float(ex[H + j]) + __bfloat162float(hx[H + j]);
