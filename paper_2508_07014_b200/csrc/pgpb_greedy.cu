@@ -35,16 +35,10 @@ struct RowDecision {
 
 // decide_row with the state's blob already loaded (issued before the row's
 // own work, so its dependent round trips overlap the top-M pass).
-template <int NC>
-__device__ __forceinline__ RowDecision decide_row_pre(const TableView &t, const float *row, int V, int blank,
-                                                      double lam, int use_boost, const BlobRegs &cur, unsigned *bm,
-                                                      float *sv, int *si, int lane) {
-  int tv[kStepTopM];
-  float tx[kStepTopM];
-  if (NC > 0)
-    warp_row_topm_thr<kStepTopM, (NC > 0 ? NC : 1)>(row, V, lane, sv, si, tv, tx);
-  else
-    warp_row_topm<kStepTopM, false>(row, V, lane, tv, tx);
+__device__ __forceinline__ RowDecision decide_topm(const TableView &t, const float *row, int V, int blank, double lam,
+                                                   int use_boost, const BlobRegs &cur, unsigned *bm,
+                                                   const int (&tv)[kStepTopM], const float (&tx)[kStepTopM],
+                                                   int lane) {
   RowDecision d{tv[0], tx[0], 0.0, 0, tv[0] == blank};
   if (!d.blank && use_boost) {
     const BCand w = blob_rerank_regs<kStepTopM>(t, cur, t.root_scores, t.root_next, t.root_next_off, bm, row, V, tv,
@@ -55,6 +49,57 @@ __device__ __forceinline__ RowDecision decide_row_pre(const TableView &t, const 
     d.next = w.nx;
   }
   return d;
+}
+
+template <int NC>
+__device__ __forceinline__ RowDecision decide_row_pre(const TableView &t, const float *row, int V, int blank,
+                                                      double lam, int use_boost, const BlobRegs &cur, unsigned *bm,
+                                                      float *sv, int *si, int lane) {
+  int tv[kStepTopM];
+  float tx[kStepTopM];
+  if (NC > 0)
+    warp_row_topm_thr<kStepTopM, (NC > 0 ? NC : 1)>(row, V, lane, sv, si, tv, tx);
+  else
+    warp_row_topm<kStepTopM, false>(row, V, lane, tv, tx);
+  return decide_topm(t, row, V, blank, lam, use_boost, cur, bm, tv, tx, lane);
+}
+
+// Log-softmax of bf16 logits into registers in the float4-chunk layout of
+// the register top-M (x[k] = elements 4 (lane + 32 k) .. + 3), written out
+// to y as well.  V % 4 == 0, 8-byte aligned logits, 16-byte aligned y.
+template <int NC>
+__device__ __forceinline__ void lsm_regs_bf16(const __nv_bfloat16 *__restrict__ x, float *__restrict__ y, int V,
+                                              int lane, float4 (&o)[NC]) {
+  const int V4 = V >> 2;
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int c = lane + 32 * k;
+    uint2 q = make_uint2(0u, 0u);
+    if (c < V4) q = __ldg(reinterpret_cast<const uint2 *>(x) + c);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&q.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&q.y));
+    o[k] = c < V4 ? make_float4(a.x, a.y, b.x, b.y) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    m = fmaxf(m, fmaxf(fmaxf(o[k].x, o[k].y), fmaxf(o[k].z, o[k].w)));
+  }
+  float mr;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(m));
+  float s = 0.0f;
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+    s += expf(o[k].x - mr) + expf(o[k].y - mr) + expf(o[k].z - mr) + expf(o[k].w - mr);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+  const float ls = logf(s);
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int c = lane + 32 * k;
+    if (c < V4) {
+      o[k] = make_float4((o[k].x - mr) - ls, (o[k].y - mr) - ls, (o[k].z - mr) - ls, (o[k].w - mr) - ls);
+      reinterpret_cast<float4 *>(y)[c] = o[k];
+    }
+  }
+  __syncwarp();  // the row may be read back by the decision (memory ordering)
 }
 
 template <int NC>
@@ -193,6 +238,8 @@ __global__ void __launch_bounds__(kThreads)
   const StepScratch sc = step_scratch(smem, V, use_boost);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const bool regs_ok = logits && (V & 3) == 0 && (ld_logits & 3) == 0 &&
+                       (reinterpret_cast<uintptr_t>(logits) & 7) == 0;
   for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < R; r += nwarps) {
     const int64_t tr = st.t[r], len = st.lengths[r];
     if (tr >= len) {  // finished utterance: nothing to decide
@@ -202,36 +249,50 @@ __global__ void __launch_bounds__(kThreads)
       }
       continue;
     }
+    // the row's bookkeeping state, loaded up front so that its round trips
+    // overlap the row's work (the R7 update below is then register-only)
+    const double am0 = st.am[r], bo0 = st.boost[r];
+    const int64_t k0 = st.k[r], n0 = st.n[r];
+    const int dur = st.durations ? st.durations[r] : -1;  // TDT duration head argmax, or RNN-T
     // the tree state's blob first: its two dependent round trips overlap
     // the row's log-softmax and top-M pass
     BlobRegs cur{};
     if (use_boost) cur = load_blob(t, __ldg(t.blob_off + st.tree[r]), lane);
     // fused joint tail: log-softmax of the row's logits, written out (the
-    // row the decision reads, and the record of what was decided on)
-    if (logits) warp_log_softmax_bf16(logits + r * ld_logits, const_cast<float *>(lp) + r * ld, V, lane);
-    const RowDecision d = decide_row_pre<NC>(t, lp + r * ld, V, blank, lam, use_boost, cur, sc.bm, sc.sv, sc.si,
-                                             lane);
+    // row the decision reads, and the record of what was decided on); with
+    // the register top-M the row's values go straight from the softmax
+    RowDecision d;
+    if (logits && NC > 0 && regs_ok) {
+      float4 x[NC > 0 ? NC : 1];
+      lsm_regs_bf16<(NC > 0 ? NC : 1)>(logits + r * ld_logits, const_cast<float *>(lp) + r * ld, V, lane, x);
+      int tv[kStepTopM];
+      float tx[kStepTopM];
+      warp_regs_topm_thr<kStepTopM, (NC > 0 ? NC : 1)>(x, V, lane, sc.sv, sc.si, tv, tx);
+      d = decide_topm(t, lp + r * ld, V, blank, lam, use_boost, cur, sc.bm, tv, tx, lane);
+    } else {
+      if (logits) warp_log_softmax_bf16(logits + r * ld_logits, const_cast<float *>(lp) + r * ld, V, lane);
+      d = decide_row_pre<NC>(t, lp + r * ld, V, blank, lam, use_boost, cur, sc.bm, sc.sv, sc.si, lane);
+    }
     if (lane == 0) {
       // R7 bookkeeping (decoding.py:371-392)
-      st.am[r] = st.am[r] + static_cast<double>(d.lp);
+      st.am[r] = am0 + static_cast<double>(d.lp);
       int64_t tn = tr;
-      const int dur = st.durations ? st.durations[r] : -1;  // TDT duration head argmax, or RNN-T
       if (d.blank) {
         tn = tr + (dur > 1 ? dur : 1);
         st.k[r] = 0;
         emit[r] = 0;
         feed[r] = st.last[r];
       } else {
-        const int64_t n = st.n[r];
+        const int64_t n = n0;
         if (n < st.lmax) {
           st.tokens[r * st.lmax + n] = d.chosen;
           st.deltas[r * st.lmax + n] = d.delta;
           st.states[r * st.lmax + n] = d.next;
         }
         st.n[r] = n + 1;
-        st.boost[r] = st.boost[r] + d.delta;
+        st.boost[r] = bo0 + d.delta;
         st.tree[r] = d.next;
-        const int64_t k = st.k[r] + 1;
+        const int64_t k = k0 + 1;
         if (dur > 0) {  // TDT: the emission also consumes dur frames
           tn = tr + dur;
           st.k[r] = 0;

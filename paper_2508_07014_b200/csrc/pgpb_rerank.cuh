@@ -465,6 +465,10 @@ namespace pgpb {
 // than 32 survivors fall back to the insertion network.  `sv`/`si` are 32
 // shared slots private to the warp.
 template <int M, int NC>
+__device__ __forceinline__ void warp_regs_topm_thr(const float4 (&x)[NC], int V, int lane, float *sv, int *si,
+                                                   int (&tv)[M], float (&tx)[M]);
+
+template <int M, int NC>
 __device__ __forceinline__ void warp_row_topm_thr(const float *__restrict__ row, int V, int lane, float *sv, int *si,
                                                   int (&tv)[M], float (&tx)[M]) {
   const float4 *row4 = reinterpret_cast<const float4 *>(row);
@@ -475,6 +479,14 @@ __device__ __forceinline__ void warp_row_topm_thr(const float *__restrict__ row,
     const int c = lane + 32 * k;
     x[k] = c < V4 ? __ldcg(row4 + c) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
   }
+  warp_regs_topm_thr<M, NC>(x, V, lane, sv, si, tv, tx);
+}
+
+// The same over a row already in registers: x[k] holds elements
+// 4 * (lane + 32 k) .. + 3 (-inf past the row's end).
+template <int M, int NC>
+__device__ __forceinline__ void warp_regs_topm_thr(const float4 (&x)[NC], int V, int lane, float *sv, int *si,
+                                                   int (&tv)[M], float (&tx)[M]) {
   float lm = -INFINITY;
   int li = INT_MAX;
 #pragma unroll
