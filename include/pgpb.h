@@ -228,6 +228,10 @@ typedef struct pgpb_label_loop_state {
    * No reference counterpart: parity-unpinned extension; with
    * d = 0 for every emission and d = 1 for blanks it is exactly R7.       */
   const int32_t *durations;
+  /* Optional (NULL: looked up): blob offset of tree[r] (TableView blob
+   * layout), carried across iterations so that a row's tree state costs one
+   * dependent load instead of two; a negative entry means "look it up". */
+  int32_t *tree_off;
 } pgpb_label_loop_state;
 
 /* One label-looping iteration fused with its bookkeeping: for every row r
@@ -258,15 +262,17 @@ int pgpb_label_loop_step_logits(const pgpb_table *table, const void *d_logits_bf
  * counterpart: the reference's transducer decoders take a host StepModel,
  * acoustic.py:203-255).  bf16 tensors, row-major.
  *  joint_hidden: z[b, :J] = relu(enc_proj[b, min(t[b], max(len[b]-1, 0)), :J]
- *                + pred_proj[b, :J]); enc_proj row stride per utterance ld_b.
+ *                + pred_proj[b, :J]); enc_proj stride per utterance ld_b,
+ *                pred_proj row stride ld_pred (elements).
  *  lstm_update:  gates = E[feed[b]] + hg[b] (E[V, 4H] = emb W_ih^T + b_ih,
  *                hg[B, 4H] = h W_hh^T + b_hh; gate order i, f, g, o), LSTM
- *                cell in fp32, h[b], c[b] overwritten iff emit[b] (NULL: all). */
+ *                cell in fp32, h[b], c[b] overwritten iff emit[b] (NULL: all);
+ *                hg row stride ld_hg (elements).                           */
 int pgpb_rnnt_joint_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, const int64_t *d_t,
-                           const int64_t *d_lengths, const void *d_pred_proj, void *d_z, int64_t B,
-                           void *stream);
-int pgpb_rnnt_lstm_update(const void *d_E, const int64_t *d_feed, const void *d_hg, const uint8_t *d_emit,
-                          void *d_h, void *d_c, int64_t B, int32_t H, void *stream);
+                           const int64_t *d_lengths, const void *d_pred_proj, int64_t ld_pred, void *d_z,
+                           int64_t B, void *stream);
+int pgpb_rnnt_lstm_update(const void *d_E, const int64_t *d_feed, const void *d_hg, int64_t ld_hg,
+                          const uint8_t *d_emit, void *d_h, void *d_c, int64_t B, int32_t H, void *stream);
 
 /* Per-state maximum of the resolved score row, max_v scores[s, v]
  * (used by the AED eos bump, decoding.py:546-552).  out[S] f32.             */

@@ -47,7 +47,7 @@ class LabelLoopState(ctypes.Structure):
 
     _fields_ = [(n, c_void_p) for n in ("t", "k", "lengths", "n", "last", "tree", "am", "boost", "tokens",
                                          "deltas", "states")] + [("lmax", c_int64), ("cap", c_int32),
-                                                                 ("durations", c_void_p)]
+                                                                 ("durations", c_void_p), ("tree_off", c_void_p)]
 
 
 class BeamHyps(ctypes.Structure):
@@ -105,8 +105,8 @@ _SIGS = {
                              POINTER(LabelLoopState), _P, _P, _P, c_void_p],
     "pgpb_label_loop_step_logits": [c_void_p, _P, c_int64, _P, c_int64, c_int32, c_int32, c_double, c_int32,
                                     POINTER(LabelLoopState), _P, _P, _P, c_void_p],
-    "pgpb_rnnt_joint_hidden": [_P, c_int64, c_int32, _P, _P, _P, _P, c_int64, c_void_p],
-    "pgpb_rnnt_lstm_update": [_P, _P, _P, _P, _P, _P, c_int64, c_int32, c_void_p],
+    "pgpb_rnnt_joint_hidden": [_P, c_int64, c_int32, _P, _P, _P, c_int64, _P, c_int64, c_void_p],
+    "pgpb_rnnt_lstm_update": [_P, _P, _P, c_int64, _P, _P, _P, c_int64, c_int32, c_void_p],
     "pgpb_beam_topk": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_int32, _P, _P, _P, _P,
                        _P, _P, _P, c_double, c_int32, c_int32, _P, _P, _P, _P, _P, _P, c_void_p],
     "pgpb_tbeam_wave": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32, c_int32,

@@ -31,6 +31,7 @@ struct RowDecision {
   double delta;
   int next;
   bool blank;
+  int noff;  // blob offset of next (boosted decisions)
 };
 
 // decide_row with the state's blob already loaded (issued before the row's
@@ -39,7 +40,7 @@ __device__ __forceinline__ RowDecision decide_topm(const TableView &t, const flo
                                                    int use_boost, const BlobRegs &cur, unsigned *bm,
                                                    const int (&tv)[kStepTopM], const float (&tx)[kStepTopM],
                                                    int lane) {
-  RowDecision d{tv[0], tx[0], 0.0, 0, tv[0] == blank};
+  RowDecision d{tv[0], tx[0], 0.0, 0, tv[0] == blank, -1};
   if (!d.blank && use_boost) {
     const BCand w = blob_rerank_regs<kStepTopM>(t, cur, t.root_scores, t.root_next, t.root_next_off, bm, row, V, tv,
                                                 tx, blank, -1, lam, t.max_root_score, lane);
@@ -47,6 +48,7 @@ __device__ __forceinline__ RowDecision decide_topm(const TableView &t, const flo
     d.lp = w.lp;
     d.delta = static_cast<double>(w.s);
     d.next = w.nx;
+    d.noff = w.noff;
   }
   return d;
 }
@@ -257,7 +259,11 @@ __global__ void __launch_bounds__(kThreads)
     // the tree state's blob first: its two dependent round trips overlap
     // the row's log-softmax and top-M pass
     BlobRegs cur{};
-    if (use_boost) cur = load_blob(t, __ldg(t.blob_off + st.tree[r]), lane);
+    if (use_boost) {
+      int so = st.tree_off ? st.tree_off[r] : -1;
+      if (so < 0) so = __ldg(t.blob_off + st.tree[r]);
+      cur = load_blob(t, so, lane);
+    }
     // fused joint tail: log-softmax of the row's logits, written out (the
     // row the decision reads, and the record of what was decided on); with
     // the register top-M the row's values go straight from the softmax
@@ -292,6 +298,7 @@ __global__ void __launch_bounds__(kThreads)
         st.n[r] = n + 1;
         st.boost[r] = bo0 + d.delta;
         st.tree[r] = d.next;
+        if (st.tree_off && use_boost) st.tree_off[r] = d.noff;
         const int64_t k = k0 + 1;
         if (dur > 0) {  // TDT: the emission also consumes dur frames
           tn = tr + dur;

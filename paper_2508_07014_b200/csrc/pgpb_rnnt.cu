@@ -24,7 +24,7 @@ namespace pgpb {
 
 __global__ void __launch_bounds__(256)
     joint_hidden_kernel(const __nv_bfloat16 *__restrict__ enc, int64_t ld_b, int J, const int64_t *__restrict__ t,
-                        const int64_t *__restrict__ lengths, const __nv_bfloat16 *__restrict__ pp,
+                        const int64_t *__restrict__ lengths, const __nv_bfloat16 *__restrict__ pp, int64_t ld_pp,
                         __nv_bfloat16 *__restrict__ z) {
   const int64_t b = blockIdx.x;
   const int64_t len = lengths[b];
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256)
   const int64_t lim = len > 0 ? len - 1 : 0;
   if (tf > lim) tf = lim;
   const __nv_bfloat16 *e = enc + b * ld_b + tf * J;
-  const __nv_bfloat16 *p = pp + b * J;
+  const __nv_bfloat16 *p = pp + b * ld_pp;
   __nv_bfloat16 *o = z + b * J;
   if ((J & 7) == 0 && ((reinterpret_cast<uintptr_t>(e) | reinterpret_cast<uintptr_t>(p) |
                         reinterpret_cast<uintptr_t>(o)) & 15) == 0) {
@@ -64,12 +64,12 @@ __device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x))
 
 __global__ void __launch_bounds__(256)
     lstm_update_kernel(const __nv_bfloat16 *__restrict__ E, const int64_t *__restrict__ feed,
-                       const __nv_bfloat16 *__restrict__ hg, const uint8_t *__restrict__ emit,
+                       const __nv_bfloat16 *__restrict__ hg, int64_t ld_hg, const uint8_t *__restrict__ emit,
                        __nv_bfloat16 *__restrict__ h, __nv_bfloat16 *__restrict__ c, int H) {
   const int64_t b = blockIdx.x;
   if (emit && !emit[b]) return;
   const __nv_bfloat16 *ex = E + feed[b] * int64_t(4 * H);
-  const __nv_bfloat16 *hx = hg + b * int64_t(4 * H);
+  const __nv_bfloat16 *hx = hg + b * ld_hg;
   if ((H & 1) == 0) {
     // two hidden units per thread (bf16x2 accesses)
     const __nv_bfloat162 *e2 = reinterpret_cast<const __nv_bfloat162 *>(ex);
@@ -109,26 +109,27 @@ __global__ void __launch_bounds__(256)
 extern "C" {
 
 int pgpb_rnnt_joint_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, const int64_t *d_t,
-                           const int64_t *d_lengths, const void *d_pred_proj, void *d_z, int64_t B, void *stream) {
+                           const int64_t *d_lengths, const void *d_pred_proj, int64_t ld_pred, void *d_z, int64_t B,
+                           void *stream) {
   using namespace pgpb;
-  if (B < 0 || J < 1 || ld_b < J) return fail(PGPB_EINVAL, "bad shape");
+  if (B < 0 || J < 1 || ld_b < J || ld_pred < J) return fail(PGPB_EINVAL, "bad shape");
   if (B == 0) return PGPB_OK;
   if (!d_enc_proj || !d_t || !d_lengths || !d_pred_proj || !d_z) return fail(PGPB_EINVAL, "NULL buffer");
   joint_hidden_kernel<<<unsigned(B), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16 *>(d_enc_proj), ld_b, J, d_t, d_lengths,
-      static_cast<const __nv_bfloat16 *>(d_pred_proj), static_cast<__nv_bfloat16 *>(d_z));
+      static_cast<const __nv_bfloat16 *>(d_pred_proj), ld_pred, static_cast<__nv_bfloat16 *>(d_z));
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }
 
-int pgpb_rnnt_lstm_update(const void *d_E, const int64_t *d_feed, const void *d_hg, const uint8_t *d_emit, void *d_h,
-                          void *d_c, int64_t B, int32_t H, void *stream) {
+int pgpb_rnnt_lstm_update(const void *d_E, const int64_t *d_feed, const void *d_hg, int64_t ld_hg,
+                          const uint8_t *d_emit, void *d_h, void *d_c, int64_t B, int32_t H, void *stream) {
   using namespace pgpb;
-  if (B < 0 || H < 1) return fail(PGPB_EINVAL, "bad shape");
+  if (B < 0 || H < 1 || ld_hg < 4 * int64_t(H)) return fail(PGPB_EINVAL, "bad shape");
   if (B == 0) return PGPB_OK;
   if (!d_E || !d_feed || !d_hg || !d_h || !d_c) return fail(PGPB_EINVAL, "NULL buffer");
   lstm_update_kernel<<<unsigned(B), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16 *>(d_E), d_feed, static_cast<const __nv_bfloat16 *>(d_hg), d_emit,
+      static_cast<const __nv_bfloat16 *>(d_E), d_feed, static_cast<const __nv_bfloat16 *>(d_hg), ld_hg, d_emit,
       static_cast<__nv_bfloat16 *>(d_h), static_cast<__nv_bfloat16 *>(d_c), H);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;

@@ -96,6 +96,10 @@ class RNNTModel:
         # input gates of every token, emb @ W_ih^T + b_ih (one GEMM per model):
         # a prediction step then gathers its row instead of embedding + GEMM
         self.E = torch.addmm(self.b_lstm, self.emb, self.w_ih.T) if dt == torch.bfloat16 else None
+        # both GEMMs that read the prediction state h, stacked: one GEMM per
+        # label iteration gives [pred_proj | hidden gates]
+        self.w_cat = torch.cat([self.w_pred, self.w_hh], 0)
+        self.b_cat = torch.cat([self.b_joint, self.b_hh], 0)
 
     def project_encoder(self, enc):
         """enc [B,T,D] -> [B,T,J] (computed once per batch)."""
@@ -170,6 +174,7 @@ class LabelLoopingDecoder:
         self.h = torch.zeros((B, model.H), device=d, dtype=model.dtype)
         self.c = torch.zeros((B, model.H), device=d, dtype=model.dtype)
         self.tree = torch.zeros(B, device=d, dtype=i32)
+        self.tree_off = torch.full((B,), -1, device=d, dtype=i32)  # blob offset of tree (-1: look up)
         self.am = torch.zeros(B, device=d, dtype=f64)
         self.boost = torch.zeros(B, device=d, dtype=f64)
         self.n = torch.zeros(B, device=d, dtype=i64)
@@ -190,7 +195,8 @@ class LabelLoopingDecoder:
         p = lambda x: x.data_ptr()  # noqa: E731
         self.state = _lib.LabelLoopState(p(self.t), p(self.k), p(self.lengths), p(self.n), p(self.last), p(self.tree),
                                          p(self.am), p(self.boost), p(self.tokens), p(self.deltas), p(self.states),
-                                         self.Lmax, self.cap, p(self.dur) if self.dur is not None else None)
+                                         self.Lmax, self.cap, p(self.dur) if self.dur is not None else None,
+                                         p(self.tree_off))
 
     # -- one label iteration (fixed kernel sequence) ------------------------
     def _iteration(self):
@@ -215,26 +221,27 @@ class LabelLoopingDecoder:
         self.c.copy_(torch.where(e2, c2, self.c))
 
     def _iteration_fused(self):
-        """The same iteration as 3 bf16 GEMMs + 3 kernels: joint hidden (frame
-        gather + add + ReLU), log-softmax fused into the boosted step
+        """The same iteration as 2 bf16 GEMMs + 3 kernels: one GEMM of h against
+        the stacked [W_pred; W_hh], joint hidden (frame gather + add + ReLU),
+        the output GEMM, log-softmax fused into the boosted step
         (pgpb_label_loop_step_logits, which writes self.lp), and the LSTM cell
         on the precomputed input gates, updating h, c of emitting rows."""
         torch, m = self.torch, self.model
         self.any_active.zero_()
-        pp = torch.addmm(m.b_joint, self.h, m.w_pred.T)
+        ph = torch.addmm(m.b_cat, self.h, m.w_cat.T)  # [B, J + 4H]: pred projection | hidden gates
+        ld = m.J + 4 * m.H
         _lib.check(_lib.LIB.pgpb_rnnt_joint_hidden(
-            self.enc_proj.data_ptr(), self.T * m.J, m.J, self.t.data_ptr(), self.lengths.data_ptr(), pp.data_ptr(),
-            self.z.data_ptr(), self.B, _lib.stream_ptr()), "pgpb_rnnt_joint_hidden")
+            self.enc_proj.data_ptr(), self.T * m.J, m.J, self.t.data_ptr(), self.lengths.data_ptr(), ph.data_ptr(),
+            ld, self.z.data_ptr(), self.B, _lib.stream_ptr()), "pgpb_rnnt_joint_hidden")
         logits = torch.addmm(m.b_out, self.z, m.w_out.T)
         _lib.check(_lib.LIB.pgpb_label_loop_step_logits(
             self.handle, logits.data_ptr(), self.V, self.lp.data_ptr(), self.B, self.V, int(m.blank_id),
             float(self.cfg.lam), int(self.use), _lib.ctypes.byref(self.state), self.emit.data_ptr(),
             self.feed.data_ptr(), self.any_active.data_ptr(), _lib.stream_ptr(),
         ), "pgpb_label_loop_step_logits")
-        hg = torch.addmm(m.b_hh, self.h, m.w_hh.T)
         _lib.check(_lib.LIB.pgpb_rnnt_lstm_update(
-            m.E.data_ptr(), self.feed.data_ptr(), hg.data_ptr(), self.emit.data_ptr(), self.h.data_ptr(),
-            self.c.data_ptr(), self.B, m.H, _lib.stream_ptr()), "pgpb_rnnt_lstm_update")
+            m.E.data_ptr(), self.feed.data_ptr(), ph.data_ptr() + 2 * m.J, ld, self.emit.data_ptr(),
+            self.h.data_ptr(), self.c.data_ptr(), self.B, m.H, _lib.stream_ptr()), "pgpb_rnnt_lstm_update")
 
     def _reset(self, enc_proj, lengths):
         torch = self.torch
@@ -248,13 +255,14 @@ class LabelLoopingDecoder:
         for x in (self.t, self.k, self.n, self.am, self.boost, self.tree, self.h, self.c):
             x.zero_()
         self.last.fill_(self.model.blank_id)
+        self.tree_off.fill_(-1)
         # initial prediction state: one step on the start symbol (blank)
         if self.fused:
             m = self.model
             hg = torch.addmm(m.b_hh, self.h, m.w_hh.T)
             _lib.check(_lib.LIB.pgpb_rnnt_lstm_update(
-                m.E.data_ptr(), self.last.data_ptr(), hg.data_ptr(), None, self.h.data_ptr(), self.c.data_ptr(),
-                self.B, m.H, _lib.stream_ptr()), "pgpb_rnnt_lstm_update")
+                m.E.data_ptr(), self.last.data_ptr(), hg.data_ptr(), 4 * m.H, None, self.h.data_ptr(),
+                self.c.data_ptr(), self.B, m.H, _lib.stream_ptr()), "pgpb_rnnt_lstm_update")
             return
         h2, c2 = self.model.lstm_step(self.last, self.h, self.c)
         self.h.copy_(h2)
