@@ -295,6 +295,15 @@ __device__ BCand blob_rerank_regs(const TableView &t, const BlobRegs &cur, const
   const bool v1 = count > 31 && lane + 32 <= count;
   BCand mine = bcand_none();
   const bool regs_ok = count <= 63;
+  // every load the fast path may need, issued together (one round trip):
+  // the closure arcs' log-probs and the argmax's root-row entries
+  const int av0 = tv[0];
+  const bool av_ok = av0 < V;
+  const float x0 = v0 ? row[b0.x] : 0.0f;
+  const float x1 = v1 ? row[b1.x] : 0.0f;
+  const float root_av = av_ok ? root[av0] : 0.0f;
+  const int rnext_av = av_ok ? rnext[av0] : 0;
+  const int rnoff_av = av_ok ? rnoff[av0] : 0;
   // Fast path.  If the stage-1 argmax a = tv[0] is a dense token (not on
   // the closure) whose root weight is the row maximum, every dense token v
   // has lp_v <= lp_a and s_v <= s_a, so (all rounded ops being monotone,
@@ -303,8 +312,8 @@ __device__ BCand blob_rerank_regs(const TableView &t, const BlobRegs &cur, const
   if (regs_ok && tv[0] < V) {
     const int av = tv[0];
     const bool in_a = __ballot_sync(kFull, (v0 && b0.x == av) || (v1 && b1.x == av)) != 0u;
-    if (!in_a && root[av] == max_root && av != ex1 && av != ex2) {
-      const float sa = acc + root[av];
+    if (!in_a && root_av == max_root && av != ex1 && av != ex2) {
+      const float sa = acc + root_av;
       const double ca = fuse(tx[0], lam, sa);
       // fp32 pre-filter: an arc whose fp32 fused score is below a's by more
       // than the fp32 rounding error of either sum cannot win; only the
@@ -313,7 +322,7 @@ __device__ BCand blob_rerank_regs(const TableView &t, const BlobRegs &cur, const
       const float ca32 = __fadd_rn(tx[0], __fmul_rn(lamf, sa));
       const float tol = 1e-4f * (fabsf(tx[0]) + fabsf(lamf * sa) + 1.0f);
       if (v0 && b0.x != ex1 && b0.x != ex2) {
-        const float x = row[b0.x];
+        const float x = x0;
         const float sv = __int_as_float(b0.z);
         const float c32 = __fadd_rn(x, __fmul_rn(lamf, sv));
         if (c32 >= ca32 - (tol + 1e-4f * (fabsf(x) + fabsf(lamf * sv)))) {
@@ -322,7 +331,7 @@ __device__ BCand blob_rerank_regs(const TableView &t, const BlobRegs &cur, const
         }
       }
       if (v1 && b1.x != ex1 && b1.x != ex2) {
-        const float x = row[b1.x];
+        const float x = x1;
         const float sv = __int_as_float(b1.z);
         const float c32 = __fadd_rn(x, __fmul_rn(lamf, sv));
         if (c32 >= ca32 - (tol + 1e-4f * (fabsf(x) + fabsf(lamf * sv)))) {
@@ -330,17 +339,17 @@ __device__ BCand blob_rerank_regs(const TableView &t, const BlobRegs &cur, const
           if (rerank_better(c, x, b1.x, ca, tx[0], av)) bcand_consider(mine, c, x, b1.x, sv, b1.y, b1.w);
         }
       }
-      if (__ballot_sync(kFull, mine.v != INT_MAX) == 0u) return BCand{ca, tx[0], av, sa, rnext[av], rnoff[av]};
+      if (__ballot_sync(kFull, mine.v != INT_MAX) == 0u) return BCand{ca, tx[0], av, sa, rnext_av, rnoff_av};
       return bcand_warp_best(mine);
     }
   }
   if (regs_ok) {
     if (v0 && b0.x != ex1 && b0.x != ex2) {
-      const float x = row[b0.x];
+      const float x = x0;
       bcand_consider(mine, fuse(x, lam, __int_as_float(b0.z)), x, b0.x, __int_as_float(b0.z), b0.y, b0.w);
     }
     if (v1 && b1.x != ex1 && b1.x != ex2) {
-      const float x = row[b1.x];
+      const float x = x1;
       bcand_consider(mine, fuse(x, lam, __int_as_float(b1.z)), x, b1.x, __int_as_float(b1.z), b1.y, b1.w);
     }
 #pragma unroll
