@@ -191,7 +191,8 @@ class TransducerBeamDecoder:
     """
 
     def __init__(self, model: StatelessTransducerModel, table: ArcTable | None, cfg: DecodeConfig, batch: int,
-                 max_frames: int, *, use_graph: bool = True, rollback: bool = False, device=None):
+                 max_frames: int, *, use_graph: bool = True, rollback: bool = False, device=None,
+                 fused: bool = True):
         torch = _torch()
         self.torch, self.model, self.table, self.cfg = torch, model, table, cfg
         if table is not None and table.vocab_size != model.V:
@@ -218,13 +219,27 @@ class TransducerBeamDecoder:
                                      self.trace.struct(), self.t.data_ptr(), self.lengths.data_ptr(), K, self.cap,
                                      self.pool_cap, int(bool(rollback)))
         self.use_graph = use_graph
+        self.fused = fused and model.dtype == torch.bfloat16
+        self.z = torch.zeros((B * K, model.J), dtype=model.dtype, device=d)
         self.graph = None
         self.launches = 0
 
     def _wave(self, k: int):
         torch, m = self.torch, self.model
-        tf = torch.minimum(self.t, (self.lengths - 1).clamp(min=0)).long()
-        self.lp.copy_(m.joint_logprobs(self.enc_proj[self.rows, tf], self.hyps.last))
+        if self.fused:
+            # joint as 1 GEMM + 2 kernels: frame gather + context gather + add
+            # + ReLU, the output GEMM, log-softmax (bf16 -> fp32 into self.lp)
+            _lib.check(_lib.LIB.pgpb_rnnt_beam_hidden(
+                self.enc_proj.data_ptr(), self.T * m.J, m.J, self.t.data_ptr(), self.lengths.data_ptr(),
+                m.pred_j.data_ptr(), self.hyps.last.data_ptr(), self.B, self.K, m.blank_id, self.z.data_ptr(),
+                _lib.stream_ptr()), "pgpb_rnnt_beam_hidden")
+            logits = torch.addmm(m.b_out, self.z, m.w_out.T)
+            _lib.check(_lib.LIB.pgpb_log_softmax_bf16(logits.data_ptr(), self.V, self.lp.data_ptr(), self.V,
+                                                      self.B * self.K, self.V, _lib.stream_ptr()),
+                       "pgpb_log_softmax_bf16")
+        else:
+            tf = torch.minimum(self.t, (self.lengths - 1).clamp(min=0)).long()
+            self.lp.copy_(m.joint_logprobs(self.enc_proj[self.rows, tf], self.hyps.last))
         _lib.check(_lib.LIB.pgpb_tbeam_wave(self.handle, self.lp.data_ptr(), self.V, self.B, self.V, m.blank_id,
                                             float(self.cfg.lam), int(self.use), k, _lib.ctypes.byref(self.state),
                                             _lib.stream_ptr()), "pgpb_tbeam_wave")

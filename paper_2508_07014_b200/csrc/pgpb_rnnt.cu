@@ -104,9 +104,79 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Stateless-transducer beam joint (beams.py): z[b, k] = relu(enc_proj[b,
+// min(t[b], len[b]-1)] + pred_j[ctx]), ctx = last[b, k] (blank when < 0),
+// one block per (b, k) row.
+__global__ void __launch_bounds__(128)
+    beam_hidden_kernel(const __nv_bfloat16 *__restrict__ enc, int64_t ld_b, int J, const int32_t *__restrict__ t,
+                       const int32_t *__restrict__ lengths, const __nv_bfloat16 *__restrict__ pred_j,
+                       const int32_t *__restrict__ last, int K, int blank, __nv_bfloat16 *__restrict__ z) {
+  const int64_t row = blockIdx.x, b = row / K;
+  const int len = lengths[b];
+  int tf = t[b];
+  const int lim = len > 0 ? len - 1 : 0;
+  if (tf > lim) tf = lim;
+  const int ctx = last[row] < 0 ? blank : last[row];
+  const __nv_bfloat16 *e = enc + b * ld_b + int64_t(tf) * J;
+  const __nv_bfloat16 *p = pred_j + int64_t(ctx) * J;
+  __nv_bfloat16 *o = z + row * J;
+  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+    const float sv = __bfloat162float(__float2bfloat16_rn(__bfloat162float(e[j]) + __bfloat162float(p[j])));
+    o[j] = __float2bfloat16_rn(sv > 0.0f ? sv : 0.0f);
+  }
+}
+
+// Row log-softmax, bf16 in, fp32 out (torch's formula order), one warp per row.
+__global__ void __launch_bounds__(256)
+    log_softmax_bf16_kernel(const __nv_bfloat16 *__restrict__ x, int64_t ldx, float *__restrict__ y, int64_t ldy,
+                            int64_t R, int V) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (r >= R) return;
+  const __nv_bfloat16 *xr = x + r * ldx;
+  float *yr = y + r * ldy;
+  float m = -INFINITY;
+  for (int v = lane; v < V; v += 32) m = fmaxf(m, __bfloat162float(xr[v]));
+  float mr;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(m));
+  float s = 0.0f;
+  for (int v = lane; v < V; v += 32) s += expf(__bfloat162float(xr[v]) - mr);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  const float ls = logf(s);
+  for (int v = lane; v < V; v += 32) yr[v] = (__bfloat162float(xr[v]) - mr) - ls;
+}
+
 }  // namespace pgpb
 
 extern "C" {
+
+int pgpb_rnnt_beam_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, const int32_t *d_t,
+                          const int32_t *d_lengths, const void *d_pred_j, const int32_t *d_last, int64_t B, int32_t K,
+                          int32_t blank, void *d_z, void *stream) {
+  using namespace pgpb;
+  if (B < 0 || J < 1 || K < 1 || ld_b < J) return fail(PGPB_EINVAL, "bad shape");
+  if (B == 0) return PGPB_OK;
+  if (!d_enc_proj || !d_t || !d_lengths || !d_pred_j || !d_last || !d_z) return fail(PGPB_EINVAL, "NULL buffer");
+  beam_hidden_kernel<<<unsigned(B * K), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16 *>(d_enc_proj), ld_b, J, d_t, d_lengths,
+      static_cast<const __nv_bfloat16 *>(d_pred_j), d_last, K, blank, static_cast<__nv_bfloat16 *>(d_z));
+  PGPB_CUDA_TRY(cudaGetLastError());
+  return PGPB_OK;
+}
+
+int pgpb_log_softmax_bf16(const void *d_x, int64_t ldx, float *d_y, int64_t ldy, int64_t R, int32_t V,
+                          void *stream) {
+  using namespace pgpb;
+  if (R < 0 || V < 1 || ldx < V || ldy < V) return fail(PGPB_EINVAL, "bad shape");
+  if (R == 0) return PGPB_OK;
+  if (!d_x || !d_y) return fail(PGPB_EINVAL, "NULL buffer");
+  log_softmax_bf16_kernel<<<unsigned((R + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16 *>(d_x), ldx, d_y, ldy, R, V);
+  PGPB_CUDA_TRY(cudaGetLastError());
+  return PGPB_OK;
+}
+
 
 int pgpb_rnnt_joint_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, const int64_t *d_t,
                            const int64_t *d_lengths, const void *d_pred_proj, int64_t ld_pred, void *d_z, int64_t B,

@@ -33,7 +33,7 @@ def _table(V, n, seed):
     return product_table(phrases, V)
 
 
-def _tbeam_case(lam, beam, cap, rollback=False, use_graph=False, B=5, T=9, V=48, seed=0):
+def _tbeam_case(lam, beam, cap, rollback=False, use_graph=False, B=5, T=9, V=48, seed=0, fused=True):
     import torch
 
     from paper_2508_07014_b200 import DecodeConfig
@@ -46,7 +46,8 @@ def _tbeam_case(lam, beam, cap, rollback=False, use_graph=False, B=5, T=9, V=48,
     enc = torch.randn((B, T, 32), generator=g, device="cuda")
     lengths = np.random.default_rng(seed).integers(1, T + 1, size=B)
     cfg = DecodeConfig(lam=lam, beam_size=beam, max_symbols_per_frame=cap)
-    dec = TransducerBeamDecoder(model, tab, cfg, B, T, use_graph=use_graph, rollback=rollback)
+    dec = TransducerBeamDecoder(model, tab, cfg, B, T, use_graph=use_graph, rollback=rollback, fused=fused)
+    assert dec.fused == fused
     out = dec.decode(model.project_encoder(enc), torch.from_numpy(lengths), record=True, want_trace=True)
     for b in range(B):
         rows = {}
@@ -75,6 +76,12 @@ def test_transducer_device_beam_matches_reference_by_replay(lam, beam, cap):
 
 def test_transducer_device_beam_rollback():
     _tbeam_case(1.0, 4, 2, rollback=True, seed=3)
+
+
+def test_transducer_device_beam_framework_joint():
+    """The framework joint (torch gathers + log_softmax) instead of the fused
+    beam-hidden and log-softmax kernels: same replay parity."""
+    _tbeam_case(1.0, 4, 2, fused=False, seed=5)
 
 
 def test_transducer_device_beam_graph_equals_eager():
