@@ -367,13 +367,26 @@ class TransformerAEDModel:
         B, Tm, d = memory.shape
         h, dh = self.h, d // self.h
         mem = memory.to(self.dtype)
+        same = getattr(self, "N", None) == B * beam and getattr(self, "B", None) == B and \
+            self.cross and self.cross[0][0].shape[2] == Tm
         self.B, self.K, self.N = B, beam, B * beam
-        self.cross = []
-        for lyr in self.layers:
+        # buffers are reused in place when the geometry repeats, so captured
+        # decode steps (AEDBeamDecoder graphs) keep valid addresses
+        if not same:
+            self.cross = []
+        for li, lyr in enumerate(self.layers):
             kv = (mem @ lyr["wkv_x"].T).view(B, Tm, 2, h, dh).permute(2, 0, 3, 1, 4)  # [2, B, h, Tm, dh]
-            self.cross.append((kv[0].contiguous(), kv[1].contiguous()))
-        self.kc = torch.zeros((self.L, self.N, h, self.max_len + 1, dh), dtype=self.dtype, device=memory.device)
-        self.vc = torch.zeros_like(self.kc)
+            if same:
+                self.cross[li][0].copy_(kv[0])
+                self.cross[li][1].copy_(kv[1])
+            else:
+                self.cross.append((kv[0].contiguous(), kv[1].contiguous()))
+        if same:
+            self.kc.zero_()
+            self.vc.zero_()
+        else:
+            self.kc = torch.zeros((self.L, self.N, h, self.max_len + 1, dh), dtype=self.dtype, device=memory.device)
+            self.vc = torch.zeros_like(self.kc)
 
     def step(self, tokens, pos: int):
         """tokens [N] (start symbol = V) at position pos -> [N, V] f32 log-probs."""
@@ -411,7 +424,7 @@ class AEDBeamDecoder:
     slots, then one pgpb_aed_step launch, then the KV-cache reorder."""
 
     def __init__(self, model: TransformerAEDModel, table: ArcTable | None, cfg: DecodeConfig, batch: int, *,
-                 max_len: int, eos: int, device=None, poll: int = 4):
+                 max_len: int, eos: int, device=None, poll: int = 4, use_graph: bool = True):
         torch = _torch()
         self.torch, self.model, self.table, self.cfg = torch, model, table, cfg
         if table is not None and table.vocab_size != model.V:
@@ -438,31 +451,52 @@ class AEDBeamDecoder:
                                    row_max.data_ptr() if row_max is not None else None, self.any_active.data_ptr(),
                                    K, max_len, eos, int(bool(cfg.eos_bump_enabled)))
         self.launches = 0
+        self.use_graph, self._warm, self.graphs = use_graph, False, {}
+        self.pool = torch.cuda.graph_pool_handle() if use_graph else None
+
+    def _step(self, n: int, records=None):
+        torch, m = self.torch, self.model
+        tokens = torch.where(self.hyps.last < 0, torch.full_like(self.hyps.last, m.V), self.hyps.last).view(-1)
+        lp = m.step(tokens, n)
+        if records is not None:
+            records.append((lp.cpu().numpy().reshape(self.B, self.K, self.V), self.hyps.host(), self.trace.host()))
+        self.any_active.zero_()
+        _lib.check(_lib.LIB.pgpb_aed_step(self.handle, lp.data_ptr(), self.V, self.B, self.V, float(self.cfg.lam),
+                                          int(self.use), _lib.ctypes.byref(self.state), _lib.stream_ptr()),
+                   "pgpb_aed_step")
+        m.reorder((self.slot_base + self.hyps.parent.long()).view(-1), n)
 
     def run(self, memory, *, record: bool = False):
+        """One batch decode.  With use_graph, the first run is eager (warm-up),
+        the second captures every step position as a CUDA graph (one shared
+        pool, replayed in capture order) and later runs replay them: a step is
+        ~60 small kernels, launch-bound when issued one by one."""
         torch, m = self.torch, self.model
         m.start(memory, self.K)
         self.hyps.reset()
         self.trace.reset()
         records = [] if record else None
         self.launches = 0
+        graphs = self.use_graph and not record and self._warm
         for n in range(self.max_len + 1):
-            tokens = torch.where(self.hyps.last < 0, torch.full_like(self.hyps.last, m.V), self.hyps.last).view(-1)
-            lp = m.step(tokens, n)
-            if record:
-                records.append((lp.cpu().numpy().reshape(self.B, self.K, self.V), self.hyps.host(),
-                                self.trace.host()))
-            self.any_active.zero_()
-            _lib.check(_lib.LIB.pgpb_aed_step(self.handle, lp.data_ptr(), self.V, self.B, self.V, float(self.cfg.lam),
-                                              int(self.use), _lib.ctypes.byref(self.state), _lib.stream_ptr()),
-                       "pgpb_aed_step")
+            if graphs:
+                g = self.graphs.get(n)
+                if g is None:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, pool=self.pool):
+                        self._step(n)
+                    self.graphs[n] = g
+                g.replay()
+            else:
+                self._step(n, records)
             self.launches += 1
-            m.reorder((self.slot_base + self.hyps.parent.long()).view(-1), n)
             if (n + 1) % self.poll == 0 or n == self.max_len:
                 self.flag_host.copy_(self.any_active, non_blocking=True)
                 torch.cuda.current_stream(self.dev).synchronize()
                 if int(self.flag_host[0]) == 0:
                     break
+        if not record:
+            self._warm = True
         return records
 
     def results(self, vocab=None, want_trace: bool = False) -> list:

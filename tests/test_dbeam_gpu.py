@@ -152,3 +152,26 @@ def test_device_beam_rejects_bad_config():
     with pytest.raises(ValueError):
         TransducerBeamDecoder(model, tab, DecodeConfig(beam_size=33), 2, 4)
     del torch
+
+
+def test_aed_device_beam_graphs_equal_eager():
+    """AED decode steps captured as CUDA graphs (second run) and replayed
+    (third run) give the eager run's n-best exactly."""
+    import torch
+
+    from paper_2508_07014_b200 import DecodeConfig
+    from paper_2508_07014_b200.beams import AEDBeamDecoder, TransformerAEDModel
+
+    V, B, max_len = 40, 4, 6
+    tab = _table(V, 100, 2100)
+    model = TransformerAEDModel(V, d_model=32, n_layers=2, n_heads=2, d_ff=64, max_len=max_len + 1, seed=2)
+    mem = torch.randn((B, 10, 32), device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+    cfg = DecodeConfig(lam=1.0, beam_size=4)
+    eager = AEDBeamDecoder(model, tab, cfg, B, max_len=max_len, eos=V - 1, use_graph=False).decode(
+        mem, want_trace=True).nbest
+    dec = AEDBeamDecoder(model, tab, cfg, B, max_len=max_len, eos=V - 1, use_graph=True)
+    runs = [dec.decode(mem, want_trace=True).nbest for _ in range(3)]  # eager warm-up, capture, replay
+    assert len(dec.graphs) > 0
+    for r in runs:
+        for x, y in zip(eager, r):
+            assert [res_tuple(a) for a in x] == [res_tuple(a) for a in y]
