@@ -371,10 +371,22 @@ __device__ BCand blob_rerank_regs(const TableView &t, const BlobRegs &cur, const
       atomicOr(bm + (tok >> 5), 1u << (tok & 31));
     }
     __syncwarp();
-    BCand full = bcand_none();
+    // Dense tokens: a token can only beat (or tie) the current winner w when
+    // fuse(x, lam, acc + max_root) >= w.c, i.e. x >= w.c - lam*(acc +
+    // max_root) up to rounding; an fp32 threshold below that (with a margin
+    // far above the rounding of either sum) skips the exact fp64 scoring of
+    // every other token.  w stays a candidate, so the result is unchanged.
+    BCand full = w;
+    float thr = -INFINITY;
+    if (w.v != INT_MAX && isfinite(w.c) && lam >= 0.0) {
+      const double sm = lam * static_cast<double>(acc + max_root);
+      const double tb = w.c - sm;
+      thr = static_cast<float>(tb - (1e-5 * (fabs(w.c) + fabs(sm)) + 1e-5));
+    }
     for (int v = lane; v < V; v += 32) {
       if (v == ex1 || v == ex2 || ((bm[v >> 5] >> (v & 31)) & 1u)) continue;
       const float x = row[v];
+      if (x < thr) continue;
       const float s = acc + root[v];
       bcand_consider(full, fuse(x, lam, s), x, v, s, rnext[v], rnoff[v]);
     }
