@@ -10,6 +10,8 @@
 // rounded fp64 ops (no FMA, as the reference's compiled code); ties break
 // toward higher raw logprob, then lower token id.
 
+#include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include <cuda_bf16.h>
@@ -446,8 +448,21 @@ static int label_loop_launch(const pgpb_table *table, const float *d_lp, int64_t
   LoopFn fn = loop_fn(nc);
   int rc = prep_kernel(fn, smem);
   if (rc) return rc;
-  const unsigned grid = static_cast<unsigned>((R + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  fn<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+  // Warps per CTA: one row per warp is latency-bound, so spread the rows
+  // over more SMs (fewer warps sharing an SM's schedulers) while the batch
+  // is small next to the GPU.  PGPB_LL_WARPS overrides (timing experiments).
+  int wpb = kWarpsPerBlock;
+  {
+    const char *ew = getenv("PGPB_LL_WARPS");
+    const int64_t nsm = sm_count(current_device());
+    if (ew) {
+      wpb = std::max(1, std::min(kWarpsPerBlock, atoi(ew)));
+    } else {
+      while (wpb > 2 && (R + wpb / 2 - 1) / (wpb / 2) <= nsm) wpb /= 2;
+    }
+  }
+  const unsigned grid = static_cast<unsigned>((R + wpb - 1) / wpb);
+  fn<<<grid, 32 * wpb, smem, static_cast<cudaStream_t>(stream)>>>(
       t, use_boost ? 1 : 0, d_lp, ld, R, V, blank, lam, *state, d_emit, d_feed, d_any_active,
       static_cast<const __nv_bfloat16 *>(d_logits), ld_logits);
   PGPB_CUDA_TRY(cudaGetLastError());
