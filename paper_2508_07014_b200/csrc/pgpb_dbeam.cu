@@ -82,7 +82,7 @@ template <int K, bool kVec>
 __device__ __forceinline__ void scan_candidates(const TableView &t, const float *root, const unsigned *bm,
                                                 int bm_words, const float *lp, int64_t ld, int64_t row0, int V,
                                                 const SBeam &s, const bool *expand, int beam, int skip, int special,
-                                                double lam, bool use_boost, Cand (&list)[K]) {
+                                                double lam, bool use_boost, const int4 *s_rec, Cand (&list)[K]) {
   for (int h = 0; h < beam; ++h) {
     if (!expand[h]) continue;
     const float *row = lp + (row0 + h) * ld;
@@ -90,7 +90,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
     float acc = 0.0f;
     int4 rec = make_int4(0, 0, 0, 0);
     if (use_boost) {
-      rec = __ldg(t.clo_rec + s.tree[h]);
+      rec = s_rec[h];  // loaded by mark_closures
       acc = __int_as_float(rec.z);
     }
     const unsigned *hbm = bm + h * bm_words;
@@ -162,17 +162,25 @@ __device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp,
 }
 
 // Mark each expandable slot's closure tokens in its bitmap.
+// Every slot's closure record is loaded at once into s_rec (reused by the
+// candidate scan), then all slots' closure tokens in one flattened pass, so
+// the marking costs two dependent round trips whatever the beam width.
 __device__ __forceinline__ void mark_closures(const TableView &t, unsigned *bm, int bm_words, const SBeam &s,
-                                              const bool *expand, int beam) {
+                                              const bool *expand, int beam, int4 *s_rec) {
   for (int i = threadIdx.x; i < beam * bm_words; i += blockDim.x) bm[i] = 0u;
+  for (int h = threadIdx.x; h < beam; h += blockDim.x)
+    s_rec[h] = expand[h] ? __ldg(t.clo_rec + s.tree[h]) : make_int4(0, 0, 0, 0);
   __syncthreads();
-  for (int h = 0; h < beam; ++h) {
-    if (!expand[h]) continue;
-    const int4 rec = __ldg(t.clo_rec + s.tree[h]);
-    for (int i = threadIdx.x; i < rec.y; i += blockDim.x) {
-      const int tok = __ldg(&t.clo[rec.x + i].x);
-      atomicOr(bm + h * bm_words + (tok >> 5), 1u << (tok & 31));
+  int total = 0;
+  for (int h = 0; h < beam; ++h) total += s_rec[h].y;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    int h = 0, off = idx;
+    while (off >= s_rec[h].y) {
+      off -= s_rec[h].y;
+      ++h;
     }
+    const int tok = __ldg(&t.clo[s_rec[h].x + off].x);
+    atomicOr(bm + h * bm_words + (tok >> 5), 1u << (tok & 31));
   }
   __syncthreads();
 }
@@ -225,6 +233,7 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SBeam s;
   __shared__ bool s_expand[kMaxTopK];
+  __shared__ int4 s_rec[kMaxTopK];
   __shared__ Cand s_warp[kBeamThreads / 32];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
@@ -288,12 +297,12 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
   if (expand_wave) {
     // 2. top-beam non-blank expansions -> next wave
     const int bm_words = (V + 31) >> 5;
-    if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam);
+    if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam, s_rec);
     Cand list[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
     scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, a.blank, -1, a.lam,
-                             use_boost, list);
+                             use_boost, s_rec, list);
     block_topk<K>(list, beam, s_warp, s_win, s_key, s_am);
     for (int r = threadIdx.x; r < beam; r += blockDim.x) {
       const int cid = s_win[r];
@@ -404,6 +413,7 @@ __global__ void __launch_bounds__(kBeamThreads) aed_step_kernel(AedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SBeam s;
   __shared__ bool s_expand[kMaxTopK];
+  __shared__ int4 s_rec[kMaxTopK];
   __shared__ Cand s_warp[kBeamThreads / 32];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
@@ -444,12 +454,12 @@ __global__ void __launch_bounds__(kBeamThreads) aed_step_kernel(AedArgs a) {
     return;
   }
   const int bm_words = (V + 31) >> 5;
-  if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam);
+  if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam, s_rec);
   Cand list[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
   scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, -1, eos, a.lam, use_boost,
-                           list);
+                           s_rec, list);
   // carried hypotheses (ended or at max_len), ranked unchanged
   for (int h = threadIdx.x; h < beam; h += blockDim.x)
     if ((s.flags[h] & kValid) && !s_expand[h])
