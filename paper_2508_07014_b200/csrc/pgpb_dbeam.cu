@@ -123,12 +123,25 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
     } else {
       for (int v = threadIdx.x; v < V; v += blockDim.x) dense(v, __ldg(row + v));
     }
-    if (use_boost) {
-      for (int i = threadIdx.x; i < rec.y; i += blockDim.x) {
-        const int4 e = __ldg(t.clo + rec.x + i);
-        if (e.x == skip || e.x == special) continue;
-        consider(e.x, __ldg(row + e.x), __dadd_rn(boost_h, static_cast<double>(__int_as_float(e.z))));
+  }
+  // closure arcs of every expandable slot in one flattened pass (their
+  // entry and log-prob loads in flight together instead of slot by slot;
+  // s_rec[h] is zero for slots that do not expand)
+  if (use_boost) {
+    int total = 0;
+    for (int h = 0; h < beam; ++h) total += s_rec[h].y;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      int h = 0, off = idx;
+      while (off >= s_rec[h].y) {
+        off -= s_rec[h].y;
+        ++h;
       }
+      const int4 e = __ldg(t.clo + s_rec[h].x + off);
+      if (e.x == skip || e.x == special) continue;
+      const float x = __ldg(lp + (row0 + h) * ld + e.x);
+      const double amv = __dadd_rn(s.am[h], static_cast<double>(x));
+      const double bv = __dadd_rn(s.boost[h], static_cast<double>(__int_as_float(e.z)));
+      list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + e.x});
     }
   }
 }
