@@ -4,14 +4,18 @@
     torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
 
 Headline (`value`): tree-advance cells/s (one cell = one (state, token)
-pair resolved: f32 score + i32 next state written), BASELINE config 5:
-20K-phrase tree (default_rng(1008) corpus, V=1024) replicated on every
-GPU, 8192 states per GPU per step (weak scaling: each rank shards its own
-8192 utterance states; no data-path collective).  A step is one advance
-launch over one resident batch of states; outputs rotate through a ring
-of 4 x 64 MiB buffers (256 MiB > 126 MB L2), so every step's writes reach
-HBM.  `e2e`: same metric through the public API with host numpy buffers
-(get_scores_batch: H2D states, kernel, D2H of both [B,V] outputs).
+pair resolved: f32 score + i32 next state written), BASELINE config 5 as
+SURVEY §8(d) states it: 20K-phrase tree (default_rng(1008) corpus, V=1024)
+replicated on every GPU, 8192 utterance states in total split into G
+contiguous shards of 8192/G (strong scaling, no data-path collective), R=8
+chained advance steps per launch (state <- next[b, tok_r[b]] from a seeded
+token stream; pgpb_advance_steps).  A step is one such launch over the
+rank's resident shard; outputs rotate over >= 256 MiB (> 126 MB L2), so
+every step's writes reach HBM.  `e2e`: the same R chained steps through the
+reference-facing API with host numpy buffers (get_scores_batch: H2D states,
+kernel, D2H of both [B,V] outputs; successor gathered on the host).
+`weak_scaling_single_step`: the previous headline (8192 states per GPU, one
+advance per launch).
 `decode_rnnt` (config 2), `decode_ctc` (greedy CTC per emission regime,
 "clean" = the reference's own decode-overhead corpus shape),
 `decode_device_beams` (configs 3 and 4, batched device beams) and
@@ -42,6 +46,8 @@ sys.path.insert(0, str(ROOT / "tests"))
 METRIC = "boosted-decode RTFx and tree-advance state·vocab/s at 20K phrases, 1/2/4/8 B200"
 UNIT = "state*vocab/s"
 B_PER_GPU = 8192
+TOTAL_STATES = 8192  # config 5: utterance states in total, sharded over the GPUs
+R_STEPS = 8  # chained advance steps per launch
 CORPUS = "p20k_v1024"
 RING = 4
 FRAME_SEC = 0.04  # acoustic.py:35
@@ -149,6 +155,24 @@ def ncu_traffic():
 # ---------------------------------------------------------------------------
 
 
+def config5(world, S, V, nph):
+    """The workload key both arms print (identical dicts at the same N)."""
+    return {
+        "workload": f"config5: {TOTAL_STATES} utterance states in total (8192/G per GPU) x {R_STEPS} chained "
+                    f"advance steps per launch (state <- next[b, tok_r[b]], seeded token stream), 20K-phrase tree "
+                    f"(S={S}) x V={V}, table replicated per GPU",
+        "total_states": TOTAL_STATES, "states_per_gpu": TOTAL_STATES // world, "chained_steps": R_STEPS,
+        "vocab": V, "num_states": S, "phrases": nph,
+        "parallelism": f"dp{world} (contiguous utterance-state shards, replicated table, no data-path collective)",
+        "l2": "outputs rotate over >= 256 MiB of (R, B, V) buffers (> 126 MB L2)",
+    }
+
+
+def shard(world, rank):
+    B = TOTAL_STATES // world
+    return rank * B, B
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -160,91 +184,67 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     tab, phrases, V = build_table()
     S = tab.num_states
-    B = args.batch
+    R = R_STEPS
+    lo, B = shard(world, rank)
     dtab = tab.device_table(local)
-    # resident inputs: a ring of state batches (each rank its own shard of utterances)
-    rng = np.random.default_rng(1000 + rank)
-    n_in = max(args.steps, 8)
-    states = torch.from_numpy(rng.integers(0, S, size=(n_in, B)).astype(np.int32)).to(dev)
-    outs = [(torch.empty((B, V), dtype=torch.float32, device=dev), torch.empty((B, V), dtype=torch.int32, device=dev))
-            for _ in range(RING)]
+    # resident inputs: the rank's contiguous shard of the 8192 utterance
+    # states (one seeded draw shared by all ranks) and a seeded token stream
+    n_in = max(args.steps, 4)
+    rng = np.random.default_rng(1000)
+    all_states = rng.integers(0, S, size=(n_in, TOTAL_STATES)).astype(np.int32)
+    all_tokens = rng.integers(0, V, size=(n_in, R, TOTAL_STATES)).astype(np.int32)
+    states = torch.from_numpy(np.ascontiguousarray(all_states[:, lo:lo + B])).to(dev)
+    tokens = torch.from_numpy(np.ascontiguousarray(all_tokens[:, :, lo:lo + B])).to(dev)
+    per_launch = R * B * V * 8
+    ring = max(2, -(-256 * 2**20 // per_launch))
+    outs = [(torch.empty((R, B, V), dtype=torch.float32, device=dev), torch.empty((R, B, V), dtype=torch.int32, device=dev))
+            for _ in range(ring)]
+    fin = torch.empty(B, dtype=torch.int32, device=dev)
+
     def step(i):
-        s, n = outs[i % RING]
-        _lib.check(_lib.LIB.pgpb_advance(dtab.handle, states[i % n_in].data_ptr(), B, s.data_ptr(), n.data_ptr(),
-                                         _lib.stream_ptr()))
+        s, n = outs[i % ring]
+        _lib.check(_lib.LIB.pgpb_advance_steps(dtab.handle, states[i % n_in].data_ptr(), tokens[i % n_in].data_ptr(),
+                                               R, B, s.data_ptr(), n.data_ptr(), None, fin.data_ptr(), 0,
+                                               _lib.stream_ptr()))
 
-    # W eager warm-up steps, then the K timed steps captured once in a CUDA
-    # graph so the device time is not host-submission bound
-    side = torch.cuda.Stream(dev)
-    side.wait_stream(torch.cuda.current_stream(dev))
-    with torch.cuda.stream(side):
-        for i in range(args.warmup):
-            step(i)
-    torch.cuda.synchronize(dev)
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        for i in range(args.steps):
-            step(i)
-    graph.replay()
-    torch.cuda.synchronize(dev)
-    stream = torch.cuda.current_stream(dev)
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        # keep the GPU under the same load for a clock window around the
-        # timed replay (nvidia-smi samples every 100 ms)
-        t_end = time.perf_counter() + 0.4
-        while time.perf_counter() < t_end:
-            graph.replay()
-            torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        start.record(stream)
-        graph.replay()
-        stop.record(stream)
-        torch.cuda.synchronize(dev)
-        t_end = time.perf_counter() + 0.4
-        while time.perf_counter() < t_end:
-            graph.replay()
-            torch.cuda.synchronize(dev)
-    ms = start.elapsed_time(stop)
+    ms, clk = _timed_graph(step, args, dev, world, clock_index=local)
     kern_ms = ms / args.steps  # average launch duration (launches back to back in the graph)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-    ms_max = float(t.item())
-    cells_total = float(B) * V * args.steps * world
-    value = cells_total / (ms_max / 1e3)
+    ms_max = _max_over_ranks(ms, dev, world)
+    value = float(TOTAL_STATES) * V * R * args.steps / (ms_max / 1e3)
 
-    # correctness spot check of the timed outputs (last ring slot) vs table semantics
-    # is covered by tests; here only make sure nothing failed
-    torch.cuda.synchronize(dev)
+    # e2e through the reference-facing API with host buffers: the same R
+    # chained steps as get_scores_batch(numpy) calls (H2D states, advance,
+    # D2H of both [B,V] outputs) and the successor gather on the host, the
+    # loop a user of the reference runs (and the reference arm times)
+    e2e_s0 = all_states[0, lo:lo + B].copy()
+    e2e_tok = all_tokens[0, :, lo:lo + B]
+    ar = np.arange(B)
 
-    # e2e through the public API with host buffers
-    e2e_states = [rng.integers(0, S, size=B).astype(np.int32) for _ in range(4)]
-    r = None
-    for i in range(3):  # same result lifetimes as the timed loop, so pinned buffers are cached
-        r = pb.get_scores_batch(tab, e2e_states[i % 4])
+    def e2e_step():
+        st = e2e_s0
+        for k in range(R):
+            r = pb.get_scores_batch(tab, st)
+            st = r.next_states[ar, e2e_tok[k]]
+        return st
+
+    e2e_step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    e2e_steps = max(3, min(args.steps, 10))
-    per_call = []
+    e2e_steps = max(2, min(args.steps, 3))
     t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        c0 = time.perf_counter()
-        r = pb.get_scores_batch(tab, e2e_states[i % 4])
-        per_call.append((time.perf_counter() - c0) * 1e3)
+    for _ in range(e2e_steps):
+        e2e_final = e2e_step()
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = float(B) * V * e2e_steps * world / float(te.item())
-    del r
+    e2e_max = _max_over_ranks(e2e_s, dev, world)
+    e2e_value = float(TOTAL_STATES) * V * R * e2e_steps / e2e_max
+    # the e2e chain must land where the device chain does
+    step(0)
+    torch.cuda.synchronize(dev)
+    e2e_ok = bool(np.array_equal(fin.cpu().numpy(), e2e_final))
 
     hbm_peak, peak_kind = peaks()
-    bytes_alg = float(B) * V * 8 + B * 4
+    bytes_alg = R * (float(B) * V * 8 + B * 4)
     achieved = bytes_alg / (kern_ms / 1e3) / 1e9
     out = {
         "metric": METRIC,
@@ -255,27 +255,27 @@ def run_ours(args, rank, world, local):
         "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32+i32 (fp32 scores, int32 next states)",
-        "data": "synthetic (seeded 20K-phrase corpus, uniform random states)",
-        "config": {
-            "workload": "config5: tree advance, 8192 states/GPU x 20K-phrase tree (S=%d) x V=%d, table replicated" % (S, V),
-            "states_per_gpu": B, "vocab": V, "num_states": S, "phrases": len(phrases),
-            "parallelism": f"dp{world} (utterance-state shards, replicated table)",
-            "l2": "outputs rotate over 4x%d MiB ring (> 126 MB L2)" % (B * V * 8 // 2**20),
-        },
+        "data": "synthetic (seeded 20K-phrase corpus, uniform random states and tokens)",
+        "config": config5(world, S, V, len(phrases)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": ncu_traffic(), "peak_kind": peak_kind,
-                     "kernel": "advance_v6_kernel", "bytes_alg_per_launch": bytes_alg,
+                     "kernel": "advance_steps_kernel", "bytes_alg_per_launch": bytes_alg,
+                     "bytes_alg_formula": "R x (B*V*8 + B*4): f32 score + i32 next per cell, i32 state per row",
                      "kernel_ms": kern_ms,
                      "timing": "CUDA events around one graph replay of the K back-to-back launches"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": B * V * 8,
-                "api": "paper_2508_07014_b200.get_scores_batch(numpy) -> C-ABI pgpb_advance_host",
-                "ms_per_call": [round(x, 3) for x in per_call]},
-        "gpu_launches": args.steps + e2e_steps,
-        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": R * B * 4,
+                "d2h_bytes_per_step": R * B * V * 8,
+                "api": "R x paper_2508_07014_b200.get_scores_batch(numpy) -> C-ABI pgpb_advance_host, "
+                       "successor gathered on the host",
+                "final_states_match_device_chain": e2e_ok},
+        "gpu_launches": args.steps + e2e_steps * R,
+        "clocks": clk,
     }
+    out["weak_scaling_single_step"] = bench_single_step(dtab, S, V, dev, rank, world, args, hbm_peak)
+    out["gpu_launches"] += out["weak_scaling_single_step"].pop("_launches", 0)
     if world == 1:
         out["advance_sweep"] = bench_advance_sweep(dtab, S, V, dev, hbm_peak)
         out["gpu_launches"] += out["advance_sweep"].pop("_launches", 0)
@@ -290,8 +290,122 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_decode:
         out["decode_beams"] = bench_beams()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(tab, B, V)
+        out["cpu_baseline"] = cpu_baseline(tab, TOTAL_STATES, V)
+    if not args.no_decode:
+        out["decode_summary"] = decode_summary(out)
     return out
+
+
+def decode_summary(out):
+    """Short top-level digest of the decode legs (boosted vs unboosted)."""
+    d = {}
+    r = out.get("decode_rnnt")
+    if r:
+        d["rnnt_greedy_cfg2"] = {"unboosted_ms": round(r["unboosted"]["ms"], 4), "boosted_ms": round(r["boosted"]["ms"], 4),
+                                 "overhead": round(r["overhead"], 4), "rtfx_boosted": round(r["boosted"]["rtfx"])}
+    c = out.get("decode_ctc", {})
+    for k, v in c.items():
+        if isinstance(v, dict) and "overhead" in v:
+            d[f"ctc_greedy_{k}"] = {"unboosted_ms": round(v["unboosted"]["ms"], 5),
+                                    "boosted_ms": round(v["boosted"]["ms"], 5), "overhead": round(v["overhead"], 4)}
+    for k, v in out.get("decode_device_beams", {}).items():
+        if isinstance(v, dict) and "overhead" in v:
+            d[k] = {"unboosted_ms": round(v["unboosted"]["ms"], 4), "boosted_ms": round(v["boosted"]["ms"], 4),
+                    "overhead": round(v["overhead"], 4)}
+    return d
+
+
+def _max_over_ranks(x, dev, world):
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    return float(t.item())
+
+
+def _timed_graph(step, args, dev, world, clock_index=None, steps=None):
+    """W eager warm-up launches, then K launches captured once in a CUDA graph
+    and replayed under CUDA events (barrier + synchronize on both sides);
+    nvidia-smi samples clocks around the timed replay."""
+    import torch
+    import torch.distributed as dist
+
+    K = args.steps if steps is None else steps
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for i in range(args.warmup):
+            step(i)
+    torch.cuda.synchronize(dev)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for i in range(K):
+            step(i)
+    graph.replay()
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = None
+    sampler = ClockSampler(clock_index) if clock_index is not None else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        # keep the GPU under the same load for a clock window around the
+        # timed replay (nvidia-smi samples every 100 ms)
+        t_end = time.perf_counter() + (0.4 if sampler else 0.0)
+        while time.perf_counter() < t_end:
+            graph.replay()
+            torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        start.record(stream)
+        graph.replay()
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+        t_end = time.perf_counter() + (0.4 if sampler else 0.0)
+        while time.perf_counter() < t_end:
+            graph.replay()
+            torch.cuda.synchronize(dev)
+    finally:
+        if sampler:
+            sampler.__exit__()
+            clk = sampler.summary()
+    del graph
+    return start.elapsed_time(stop), clk
+
+
+def bench_single_step(dtab, S, V, dev, rank, world, args, hbm_peak, B=8192):
+    """Previous headline form: weak scaling, 8192 states per GPU, one
+    advance (advance_v6_kernel) per launch, outputs over a 4 x 64 MiB ring."""
+    import torch
+
+    from paper_2508_07014_b200 import _lib
+
+    rng = np.random.default_rng(1000 + rank)
+    n_in = max(args.steps, 8)
+    states = torch.from_numpy(rng.integers(0, S, size=(n_in, B)).astype(np.int32)).to(dev)
+    outs = [(torch.empty((B, V), dtype=torch.float32, device=dev), torch.empty((B, V), dtype=torch.int32, device=dev))
+            for _ in range(RING)]
+
+    def step(i):
+        s, n = outs[i % RING]
+        _lib.check(_lib.LIB.pgpb_advance(dtab.handle, states[i % n_in].data_ptr(), B, s.data_ptr(), n.data_ptr(),
+                                         _lib.stream_ptr()))
+
+    ms, _ = _timed_graph(step, args, dev, world)
+    ms_max = _max_over_ranks(ms, dev, world)
+    kern_ms = ms / args.steps
+    gbs = (B * V * 8 + B * 4) / (kern_ms / 1e3) / 1e9
+    res = {"workload": f"one advance of {B} states per GPU per launch (weak scaling), advance_v6_kernel",
+           "value": float(B) * V * args.steps * world / (ms_max / 1e3), "unit": UNIT, "ms_per_launch": kern_ms,
+           "GBps": gbs, "frac_hbm": gbs / hbm_peak, "_launches": args.warmup + 2 * args.steps}
+    del outs
+    torch.cuda.empty_cache()
+    return res
 
 
 def _ctc_regimes(B, T, V, dev, rank):
@@ -384,29 +498,22 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
     return out
 
 
-def bench_advance_sweep(dtab, S, V, dev, hbm_peak, batches=(128, 1024, 8192, 65536), steps=20):
-    """SURVEY 8(d) batch sweep of the advance on one GPU: K back-to-back
-    launches in one graph over an output ring larger than L2 (>= 256 MiB),
-    uniform random states; device time per launch and the fraction of the
-    measured HBM peak (8 B per cell + 4 B per state)."""
+def bench_advance_sweep(dtab, S, V, dev, hbm_peak, batches=(128, 1024, 8192, 65536), steps=20, R=R_STEPS):
+    """SURVEY 8(d) batch sweep of the advance on one GPU, uniform random
+    states: `single` = one advance per launch (advance_v6_kernel), `chained`
+    = R chained steps per launch (advance_steps_kernel); K back-to-back
+    launches in one graph over an output ring larger than L2 (>= 256 MiB);
+    device time per launch and the fraction of the measured HBM peak
+    (8 B per cell + 4 B per state row)."""
     import torch
 
     from paper_2508_07014_b200 import _lib
 
     rng = np.random.default_rng(77)
-    res = {"note": "graph of %d launches per batch, outputs rotate over >= 256 MiB" % steps, "_launches": 0}
-    for B in batches:
-        per = B * V * 8
-        ring = max(2, min(steps, -(-256 * 2**20 // per)))
-        states = torch.from_numpy(rng.integers(0, S, size=(steps, B)).astype(np.int32)).to(dev)
-        outs = [(torch.empty((B, V), dtype=torch.float32, device=dev), torch.empty((B, V), dtype=torch.int32, device=dev))
-                for _ in range(ring)]
+    res = {"note": "graph of %d launches per batch and form, outputs rotate over >= 256 MiB; chained: R=%d steps "
+                   "per launch" % (steps, R), "_launches": 0}
 
-        def step(i):
-            sc, nx = outs[i % ring]
-            _lib.check(_lib.LIB.pgpb_advance(dtab.handle, states[i].data_ptr(), B, sc.data_ptr(), nx.data_ptr(),
-                                             _lib.stream_ptr()))
-
+    def timed(step):
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
@@ -428,12 +535,38 @@ def bench_advance_sweep(dtab, S, V, dev, hbm_peak, batches=(128, 1024, 8192, 655
             torch.cuda.synchronize(dev)
             ms = a.elapsed_time(b) / steps
             best = ms if best is None else min(best, ms)
-        gbs = (B * V * 8 + B * 4) / (best / 1e3) / 1e9
-        res[str(B)] = {"ms_per_launch": best, "cells_per_s": B * V / (best / 1e3), "GBps": gbs,
-                       "frac_hbm": gbs / hbm_peak}
         res["_launches"] += 3 + 4 * steps
-        del outs, states, g
-        torch.cuda.empty_cache()
+        return best
+
+    for B in batches:
+        states = torch.from_numpy(rng.integers(0, S, size=(steps, B)).astype(np.int32)).to(dev)
+        entry = {}
+        for form, r in (("single", 1), ("chained", R)):
+            per = r * B * V * 8
+            ring = max(2, min(steps, -(-256 * 2**20 // per)))
+            outs = [(torch.empty((r, B, V), dtype=torch.float32, device=dev),
+                     torch.empty((r, B, V), dtype=torch.int32, device=dev)) for _ in range(ring)]
+            if r == 1:
+                def step(i):
+                    sc, nx = outs[i % ring]
+                    _lib.check(_lib.LIB.pgpb_advance(dtab.handle, states[i].data_ptr(), B, sc.data_ptr(),
+                                                     nx.data_ptr(), _lib.stream_ptr()))
+            else:
+                toks = torch.from_numpy(rng.integers(0, V, size=(r, B)).astype(np.int32)).to(dev)
+
+                def step(i):
+                    sc, nx = outs[i % ring]
+                    _lib.check(_lib.LIB.pgpb_advance_steps(dtab.handle, states[i].data_ptr(), toks.data_ptr(), r, B,
+                                                           sc.data_ptr(), nx.data_ptr(), None, None, 0,
+                                                           _lib.stream_ptr()))
+            best = timed(step)
+            gbs = r * (B * V * 8 + B * 4) / (best / 1e3) / 1e9
+            entry[form] = {"ms_per_launch": best, "cells_per_s": r * B * V / (best / 1e3), "GBps": gbs,
+                           "frac_hbm": gbs / hbm_peak}
+            del outs
+            torch.cuda.empty_cache()
+        res[str(B)] = entry
+        del states
     return res
 
 
@@ -672,7 +805,7 @@ def _ref_module():
     return (mod, "reference") if mod is not None else (None, "port")
 
 
-def _cpu_advance(tab, states, threads):
+def _cpu_advance(tab, states, threads, want_next=False):
     """Advance on host cores: reference kernel (oracle/_ref) or the oracle port,
     batch sharded over a thread pool (the kernels release the GIL), as the
     reference CLI's --workers pool does (cli.py:302-310)."""
@@ -688,7 +821,9 @@ def _cpu_advance(tab, states, threads):
     else:
         fn = lambda s: orc.score_batch(tab, s)  # noqa: E731
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(fn, shards))
+        outs = list(ex.map(fn, shards))
+    if want_next:
+        return np.concatenate([o[1] for o in outs], axis=0)
     return kind
 
 
@@ -728,29 +863,54 @@ def _cpu_model():
 
 
 def run_reference(args, rank, world):
+    """The reference's own CPU implementation of the config-5 workload on the
+    host cores: its compiled kernel (oracle/_ref = /root/reference's
+    _kernels.pyx built by oracle/build_ref.py; the C oracle port when absent)
+    on a table built by the oracle's restatement of the reference's tree
+    build (bit-identical arrays; nothing from paper_2508_07014_b200 is
+    imported on this path).  Each step = the R chained advances of the
+    8192 utterance states (score_batch sharded over all host threads, as the
+    reference CLI's --workers pool does, then the successor gather)."""
     if rank != 0:
         return None
-    tab, phrases, V = build_table()
-    B = args.batch
+    import gen_inputs as gi
+    from oracle import oracle as orc
+
+    phrases, V = gi.corpus(CORPUS)
+    tab = orc.build_table(phrases, V)
+    S = tab.num_states
+    B, R = TOTAL_STATES, R_STEPS
     threads = os.cpu_count() or 1
     rng = np.random.default_rng(1000)
-    st = [rng.integers(0, tab.num_states, size=B).astype(np.int32) for _ in range(4)]
+    n_in = max(args.steps, 4)
+    all_states = rng.integers(0, S, size=(n_in, TOTAL_STATES)).astype(np.int32)
+    all_tokens = rng.integers(0, V, size=(n_in, R, TOTAL_STATES)).astype(np.int32)
+    ar = np.arange(B)
+
+    def step(i):
+        st = all_states[i % n_in]
+        for k in range(R):
+            nx = _cpu_advance(tab, st, threads, want_next=True)
+            st = nx[ar, all_tokens[i % n_in, k]]
+        return st
+
     for i in range(args.warmup):
-        kind = _cpu_advance(tab, st[i % 4], threads)
+        step(i)
     kind = _ref_module()[1]
     t0 = time.perf_counter()
     for i in range(args.steps):
-        _cpu_advance(tab, st[i % 4], threads)
+        step(i)
     el = time.perf_counter() - t0
-    value = args.steps * B * V / el
+    value = args.steps * B * V * R / el
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic (seeded 20K-phrase corpus, uniform random states)",
-        "config": {"workload": "config5: tree advance, %d states x 20K-phrase tree x V=%d on host cores" % (B, V),
-                   "states_per_step": B, "vocab": V, "num_states": tab.num_states},
+        "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32+i32 (fp32 scores, int32 next states)",
+        "data": "synthetic (seeded 20K-phrase corpus, uniform random states and tokens)",
+        "config": config5(world, S, V, len(phrases)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"each step = one full {B}-state advance sharded over {threads} threads",
+                         "sample": f"each step = {R} chained {B}-state advances (score_batch sharded over {threads} "
+                                   "threads + successor gather), the whole config-5 workload",
                          "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

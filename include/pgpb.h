@@ -143,6 +143,20 @@ int pgpb_advance(const pgpb_table *table, const int32_t *d_states, int64_t batch
 int pgpb_advance_host(const pgpb_table *table, const int32_t *h_states, int64_t batch,
                       float *h_scores, int32_t *h_next, void *stream);
 
+/* R chained advances in one launch (BASELINE config 5):
+ * s_0 = d_states[b]; step k advances s_k exactly as pgpb_advance does and
+ * writes d_scores/d_next[(k*B + b)*V + v] (R x [B,V] outputs); then
+ * s_{k+1} = next_k[b, d_tokens[k*B + b]].  Optional outputs: d_trace[k*B + b]
+ * = s_k (R x B), d_final_states[b] = s_R.  `parts` = column parts per row
+ * (0 = choose; a power of two dividing the row into multiples of 128
+ * tokens).  Tokens and states are not range-checked on device.
+ * Each step is the reference's get_scores_batch (table.py:190-214,
+ * _kernels.pyx:30-72) of that step's states; the successor rule is the
+ * reference's next-state lookup (decoding.py:379-383, _kernels.pyx:204-209). */
+int pgpb_advance_steps(const pgpb_table *table, const int32_t *d_states, const int32_t *d_tokens,
+                       int32_t steps, int64_t batch, float *d_scores, int32_t *d_next, int32_t *d_trace,
+                       int32_t *d_final_states, int32_t parts, void *stream);
+
 /* Reference chain-walk advance (no flattened closure): walks failure arcs
  * per row exactly as _kernels.pyx:56-71.  Same outputs as pgpb_advance;
  * kept for tables whose closure would not fit and as a cross-check.        */

@@ -94,6 +94,7 @@ _SIGS = {
     "pgpb_advance": [c_void_p, _P, c_int64, _P, _P, c_void_p],
     "pgpb_advance_host": [c_void_p, _P, c_int64, _P, _P, c_void_p],
     "pgpb_advance_chain": [c_void_p, _P, c_int64, _P, _P, c_void_p],
+    "pgpb_advance_steps": [c_void_p, _P, _P, c_int32, c_int64, _P, _P, _P, _P, c_int32, c_void_p],
     "pgpb_ctc_greedy": [c_void_p, _P, c_int64, c_int64, c_int32, _P, c_int32, c_double, c_int32,
                         _P, _P, _P, _P, _P, _P, c_void_p],
     "pgpb_ctc_greedy_host": [c_void_p, _P, c_int64, c_int32, c_int32, c_double, c_int32, _P, _P, _P,

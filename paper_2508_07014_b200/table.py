@@ -359,6 +359,59 @@ def advance(table: ArcTable, states, **kw) -> ScoreQueryResult:
     return get_scores_batch(table, states, **kw)
 
 
+@dataclass(frozen=True)
+class AdvanceStepsResult:
+    """R chained advances: scores / next_states (R, B, V), the state each step
+    queried (trace, (R, B)) and the state after the last step (final, (B,))."""
+
+    scores: object
+    next_states: object
+    trace: object
+    final_states: object
+
+
+def advance_steps(table, states, tokens, *, parts: int = 0, out=None, check: bool = True) -> AdvanceStepsResult:
+    """R chained advances in one launch (pgpb_advance_steps, BASELINE config 5):
+    step k = get_scores_batch of the step's states (table.py:190-214);
+    s_{k+1}[b] = next_k[b, tokens[k, b]] (the reference's next-state lookup,
+    decoding.py:379-383).  `states` int32 (B,) and `tokens` int32 (R, B) CUDA
+    tensors; outputs are device tensors on torch's current stream."""
+    import torch
+
+    if not (_is_tensor(states) and states.is_cuda and _is_tensor(tokens) and tokens.is_cuda):
+        raise ValueError("advance_steps takes CUDA tensors (states (B,), tokens (R, B))")
+    st = states.reshape(-1).to(torch.int32).contiguous()
+    tk = tokens.to(torch.int32).contiguous()
+    B, V = st.shape[0], table.vocab_size
+    if tk.dim() != 2 or tk.shape[1] != B:
+        raise ValueError("tokens must be (R, B)")
+    R = tk.shape[0]
+    if check and B:
+        lo, hi = torch.aminmax(st)
+        if int(lo) < 0 or int(hi) >= table.num_states:
+            raise IndexError(f"state id out of range [0, {table.num_states})")
+        if R:
+            lo, hi = torch.aminmax(tk)
+            if int(lo) < 0 or int(hi) >= V:
+                raise IndexError(f"token id out of range [0, {V})")
+    dev_ = st.device
+    if out is None:
+        scores = torch.empty((R, B, V), dtype=torch.float32, device=dev_)
+        nxt = torch.empty((R, B, V), dtype=torch.int32, device=dev_)
+    else:
+        scores, nxt = out
+        if tuple(scores.shape) != (R, B, V) or tuple(nxt.shape) != (R, B, V):
+            raise ValueError("out buffers must be (R, B, V)")
+    trace = torch.empty((R, B), dtype=torch.int32, device=dev_)
+    final = st.clone()
+    if B and R:
+        dt = table.device_table(dev_.index)
+        _lib.check(_lib.LIB.pgpb_advance_steps(dt.handle, st.data_ptr(), tk.data_ptr(), R, B, scores.data_ptr(),
+                                               nxt.data_ptr(), trace.data_ptr(), final.data_ptr(), int(parts),
+                                               _lib.stream_ptr()), "pgpb_advance_steps")
+    return AdvanceStepsResult(scores=scores, next_states=nxt, trace=trace, final_states=final)
+
+
 def naive_score(tree: PrefixTree, state: int, token: int, unk_score: float = 0.0) -> tuple[float, int]:
     """Single-cell resolution on the trie itself (table.py:217-247), fp32 like compile."""
     if not 0 <= state < tree.num_nodes:

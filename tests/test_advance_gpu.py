@@ -63,25 +63,110 @@ def test_advance_corpora_match_reference_golden(name):
     assert np.array_equal(c.next_states.cpu().numpy(), res.next_states)
 
 
-@pytest.mark.parametrize("variant", ["6", "7", "5", "3", "2", "1"])
+@pytest.mark.parametrize("chain", [False, True])
 @pytest.mark.parametrize("name,B", [("p20k_v1024", 8192), ("p20k_v4096", 2048), ("p5k_v1024", 3000),
-                                    ("p20k_v1024", 37)])
-def test_advance_full_size_vs_oracle(name, B, variant, monkeypatch):
-    """Every advance kernel variant (PGPB_ADVANCE_VARIANT; 6 is the default)
-    bit-exact against the oracle."""
+                                    ("p20k_v1024", 37), ("p20k_v1024", 1024), ("p20k_v1024", 65)])
+def test_advance_full_size_vs_oracle(name, B, chain):
+    """The production advance (and the reference chain-walk kernel)
+    bit-exact against the oracle at the benchmark sizes."""
     import torch
 
-    from paper_2508_07014_b200 import get_scores_batch
+    from paper_2508_07014_b200.table import _advance_device
 
-    monkeypatch.setenv("PGPB_ADVANCE_VARIANT", variant)
     phrases, V = gi.corpus(name)
     tab = product_table(phrases, V)
     rng = np.random.default_rng(B)
     states = rng.integers(0, tab.num_states, size=B).astype(np.int32)
-    d = get_scores_batch(tab, torch.from_numpy(states).cuda())
+    d = _advance_device(tab, torch.from_numpy(states).cuda(), check=True, out=None, chain=chain)
     sc, nx = orc.score_batch(tab, states)
     assert bits_equal(d.scores.cpu().numpy(), sc)
     assert np.array_equal(d.next_states.cpu().numpy(), nx)
+
+
+def _closure_biased_tokens(tab, states0, R, rng, p_closure=0.6):
+    """Token stream for R chained steps where about p_closure of the steps
+    take a first-hit (closure) arc of the current state, so the successor
+    lookup exercises the entry path, not only the dense root row."""
+    V = tab.vocab_size
+    toks = np.empty((R, states0.size), np.int32)
+    s = states0.copy()
+    for k in range(R):
+        sc, nx = orc.score_batch(tab, s)
+        for b in range(s.size):
+            over = np.nonzero(nx[b] != tab.root_next)[0] if rng.random() < p_closure else np.empty(0)
+            toks[k, b] = int(rng.choice(over)) if over.size else int(rng.integers(0, V))
+        s = nx[np.arange(s.size), toks[k]].astype(np.int32)
+    return toks
+
+
+@pytest.mark.parametrize("name,B,R,parts", [("p20k_v1024", 1024, 6, 0), ("p20k_v1024", 1024, 4, 1),
+                                            ("p20k_v1024", 300, 5, 2), ("p20k_v1024", 97, 3, 8),
+                                            ("p20k_v1024", 8192, 2, 0), ("p20k_v4096", 256, 3, 0),
+                                            ("p5k_v1024", 4, 7, 0)])
+def test_advance_steps_vs_oracle(name, B, R, parts):
+    """Chained R-step advance (config 5): every step's rows bit-exact vs the
+    oracle advance of that step's states, and s_{k+1} = next_k[b, tok_k[b]]."""
+    import torch
+
+    from paper_2508_07014_b200 import advance_steps
+
+    phrases, V = gi.corpus(name)
+    tab = product_table(phrases, V)
+    rng = np.random.default_rng(B * 31 + R)
+    s0 = rng.integers(0, tab.num_states, size=B).astype(np.int32)
+    if B <= 1024:
+        toks = _closure_biased_tokens(tab, s0, R, rng)
+    else:
+        toks = rng.integers(0, V, size=(R, B)).astype(np.int32)
+    r = advance_steps(tab, torch.from_numpy(s0).cuda(), torch.from_numpy(toks).cuda(), parts=parts)
+    tr = r.trace.cpu().numpy()
+    assert np.array_equal(tr[0], s0)
+    s = s0
+    for k in range(R):
+        assert np.array_equal(tr[k], s), f"step {k} states"
+        sc, nx = orc.score_batch(tab, s)
+        assert bits_equal(r.scores[k].cpu().numpy(), sc), f"step {k} scores"
+        assert np.array_equal(r.next_states[k].cpu().numpy(), nx), f"step {k} next"
+        s = nx[np.arange(B), toks[k]].astype(np.int32)
+    assert np.array_equal(r.final_states.cpu().numpy(), s)
+
+
+@pytest.mark.parametrize("V", [130, 28])
+def test_advance_steps_generic_path(V):
+    """Vocabularies the chained kernel cannot split (V % 128 != 0) take R
+    single-step launches plus a successor gather: same contract."""
+    import torch
+
+    from paper_2508_07014_b200 import advance_steps
+
+    rng = np.random.default_rng(V)
+    tab = product_table(gi.random_phrase_set(rng, 40, 8, V), V, unk=0.1)
+    B, R = 33, 4
+    s0 = rng.integers(0, tab.num_states, size=B).astype(np.int32)
+    toks = _closure_biased_tokens(tab, s0, R, rng)
+    r = advance_steps(tab, torch.from_numpy(s0).cuda(), torch.from_numpy(toks).cuda())
+    s = s0
+    for k in range(R):
+        sc, nx = orc.score_batch(tab, s)
+        assert np.array_equal(r.trace[k].cpu().numpy(), s)
+        assert bits_equal(r.scores[k].cpu().numpy(), sc) and np.array_equal(r.next_states[k].cpu().numpy(), nx)
+        s = nx[np.arange(B), toks[k]].astype(np.int32)
+    assert np.array_equal(r.final_states.cpu().numpy(), s)
+
+
+def test_advance_steps_edge_cases(fig_table):
+    import torch
+
+    from paper_2508_07014_b200 import advance_steps
+
+    z = torch.zeros(0, dtype=torch.int32, device="cuda")
+    r = advance_steps(fig_table, z, torch.zeros((3, 0), dtype=torch.int32, device="cuda"))
+    assert r.scores.shape == (3, 0, fig_table.vocab_size)
+    with pytest.raises(IndexError):
+        advance_steps(fig_table, torch.tensor([0], device="cuda"),
+                      torch.tensor([[fig_table.vocab_size]], device="cuda"))
+    with pytest.raises(ValueError):
+        advance_steps(fig_table, torch.tensor([0, 1], device="cuda"), torch.tensor([[1]], device="cuda"))
 
 
 def test_advance_properties_at_64k_rows():
