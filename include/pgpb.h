@@ -46,6 +46,14 @@ extern "C" {
 const char *pgpb_last_error(void);
 int pgpb_abi_version(void);
 
+/* Code-path overrides for tests and measurements; value 0 restores the
+ * automatic choice.  Keys: "ctc.consumers" (walker warps per CTA),
+ * "ctc.segment" (frames per walker segment), "ctc.seq" (1 = sequential walk,
+ * 2 = speculative rounds only), "ll.warps" (label-loop rows per CTA).  Every
+ * setting selects between bit-identical code paths; process-wide, not
+ * thread-safe against concurrent launches.  PGPB_EINVAL on an unknown key. */
+int pgpb_set_tuning(const char *key, int32_t value);
+
 /* ------------------------------------------------------------------------
  * Tree compilation (host code, C++).  Replaces the Python loops of
  *   build_prefix_tree   tree.py:145-186
@@ -296,6 +304,11 @@ int pgpb_log_softmax_bf16(const void *d_x, int64_t ldx, float *d_y, int64_t ldy,
                           void *stream);
 int pgpb_rnnt_lstm_update(const void *d_E, const int64_t *d_feed, const void *d_hg, int64_t ld_hg,
                           const uint8_t *d_emit, void *d_h, void *d_c, int64_t B, int32_t H, void *stream);
+
+/* Per state: final_score[s] when is_final[s], else 0 (f32[S]) — the final
+ * part of the AED eos bump (decoding.py:546-552), for tables that live only
+ * on the device (load_table_device).                                        */
+int pgpb_final_bonus(const pgpb_table *table, float *d_out, void *stream);
 
 /* Per-state maximum of the resolved score row, max_v scores[s, v]
  * (used by the AED eos bump, decoding.py:546-552).  out[S] f32.             */

@@ -82,6 +82,7 @@ class AedState(ctypes.Structure):
 _P = c_void_p
 _SIGS = {
     "pgpb_abi_version": [],
+    "pgpb_set_tuning": [ctypes.c_char_p, c_int32],
     "pgpb_trie_build": [_P, _P, c_int64, c_int32, c_double, c_double, c_int32, c_double, c_int64,
                         _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "pgpb_trie_fail_links": [c_int64, _P, _P, c_int32, _P],
@@ -102,6 +103,7 @@ _SIGS = {
     "pgpb_greedy_step": [c_void_p, _P, c_int64, c_int64, c_int32, _P, _P, c_int32, c_double, c_int32,
                          _P, _P, _P, _P, _P, c_void_p],
     "pgpb_row_max": [c_void_p, _P, c_void_p],
+    "pgpb_final_bonus": [c_void_p, _P, c_void_p],
     "pgpb_label_loop_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32,
                              POINTER(LabelLoopState), _P, _P, _P, c_void_p],
     "pgpb_label_loop_step_logits": [c_void_p, _P, c_int64, _P, c_int64, c_int32, c_int32, c_double, c_int32,
@@ -192,6 +194,11 @@ def require_cuda() -> None:
         raise RuntimeError(
             "paper_2508_07014_b200 needs a CUDA device (sm_100a); there is no CPU fallback"
         )
+
+
+def set_tuning(key: str, value: int) -> None:
+    """Code-path override (pgpb_set_tuning); 0 = automatic.  Tests only."""
+    check(LIB.pgpb_set_tuning(key.encode(), int(value)), "pgpb_set_tuning")
 
 
 def abi_version() -> int:

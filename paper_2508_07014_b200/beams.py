@@ -32,6 +32,7 @@ import numpy as np
 
 from . import _lib
 from .decoding import DecodeConfig, DecodeResult, TraceStep, _boost_active, _text
+from .rnnt import _check_lengths
 from .table import ArcTable
 
 VALID, ENDED = 1, 2
@@ -259,6 +260,7 @@ class TransducerBeamDecoder:
             raise ValueError("batch geometry differs from the decoder's")
         self.enc_proj[:, :T].copy_(enc_proj)
         ln = torch.as_tensor(lengths, device=self.dev) if lengths is not None else torch.full((B,), T, device=self.dev)
+        _check_lengths(ln, B, T)
         self.lengths.copy_(ln.to(torch.int32))
         self.hyps.reset()
         self.pool.reset()

@@ -471,7 +471,6 @@ struct Args {
   int use_boost;
   int TS;        // frames per segment
   int seq_mode;  // 0 auto, 1 always sequential, 2 never
-  int stop;      // timing experiments only (PGPB_CTC_STOP): return after stage `stop` (outputs invalid)
   int32_t *tokens;
   double *deltas;
   int32_t *ostates;
@@ -1148,7 +1147,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
   CF_MARK(0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   CF_MARK(1);
-  if (g.stop == 1) return;
   Ctx x;
   x.t = &t;
   x.s = &s;
@@ -1170,7 +1168,9 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
       cf_rep = 1;
     }
 #endif
-    const int64_t Tb = g.lengths ? int64_t(__ldg(g.lengths + b)) : g.T;
+    // lengths are clamped to [0, T] so a bad length cannot address another
+    // utterance's rows or outputs (the host layer rejects them first)
+    const int64_t Tb = g.lengths ? min(max(int64_t(__ldg(g.lengths + b)), int64_t(0)), g.T) : g.T;
     __syncthreads();
     if (threadIdx.x == 0) {
       s.misc[0] = root_off;
@@ -1210,7 +1210,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
       }
       __syncthreads();
       CF_MARK(2);
-      if (g.stop == 2) return;
       // One pass of every walker lane over its chunk: the argmax emissions
       // (for the round-0 guesses) and the mode counts.
       //
@@ -1302,7 +1301,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         seq = g.seq_mode == 1 || (g.seq_mode == 0 && 4 * ts > tc && tc >= 8);
         CF_MARK(3);
       }
-      if (g.stop == 3) return;
       if (boost && seq) {
         // ---- sequential mode: warp 0 walks the segment ----
         x.rows = rows;
@@ -1343,7 +1341,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         s.c_sst[c] = st;
         s.c_slast[c] = last;
         CF_MARK(4);
-        if (g.stop == 4) return;
 #ifdef PGPB_SEQ_PROFILE
         const long long t_r0 = clock64();
 #endif
@@ -1361,7 +1358,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         s.c_est[c] = st;
         s.c_elast[c] = last;
         CF_MARK(5);
-        if (g.stop == 5) return;
 #ifdef PGPB_SEQ_PROFILE
         if (lane == 0 && wid < W) {
           const unsigned long long d = clock64() - t_r0;
@@ -1447,7 +1443,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
       }
       __syncthreads();
       CF_MARK(6);
-      if (g.stop == 6) return;
       // ---- tail: one pass over each thread's contiguous frames (emit
       // count, exact-sum partials of am and boost),
       // warp scans / reductions, one barrier, then compaction ----
@@ -1482,7 +1477,6 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
       }
       __syncthreads();
       CF_MARK(7);
-      if (g.stop == 7) return;
       int pos = base + incl - cntm;
       for (int w = 0; w < wid; ++w) pos += s.wsum[w];
       int32_t *otok = g.tokens + b * g.T;
@@ -1563,8 +1557,7 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
   if (F > 0) {
     // one wave: 2 resident CTAs per SM (<= 128 registers), grid-stride over
     // frame pairs (0.5 us faster than 8 waves of CTAs on 128 x 200 frames)
-    const char *eps = getenv("PGPB_CTC_A_PERSM");  // timing experiments
-    const unsigned grid = warp_grid((F + 1) / 2, eps ? std::max(1, atoi(eps)) : 2);
+    const unsigned grid = warp_grid((F + 1) / 2, 2);
     using KA = void (*)(const float *, int64_t, int64_t, int, const int32_t *, int, int4 *);
     KA ka = use_boost ? (vec ? frame_top2_kernel<true, true> : frame_top2_kernel<true, false>)
                       : (vec ? frame_top2_kernel<false, true> : frame_top2_kernel<false, false>);
@@ -1574,11 +1567,6 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
       cudaFreeAsync(top, st);
       return fail(PGPB_ECUDA, std::string("frame_top2_kernel: ") + cudaGetErrorString(e));
     }
-  }
-  const char *eoa = getenv("PGPB_CTC_ONLY_A");  // timing experiments: phase A alone (outputs invalid)
-  if (eoa && atoi(eoa) == 1) {
-    if (top) cudaFreeAsync(top, st);
-    return PGPB_OK;
   }
   Args a{};
   a.t = table ? table->view : empty_view(V);
@@ -1603,11 +1591,10 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
     const int64_t want = (T + 31) / 32;
     W = int(want < 1 ? 1 : (want > kMaxConsumers ? kMaxConsumers : want));
   }
-  const char *ew = getenv("PGPB_CTC_CONSUMERS");
-  if (ew) W = std::max(1, std::min(kMaxConsumers, atoi(ew)));
+  const Tuning &tun = tuning();
+  if (tun.ctc_consumers) W = std::max(1, std::min(kMaxConsumers, tun.ctc_consumers));
   int TS = int(T < 1 ? 1 : (T > 8192 ? 8192 : T));
-  const char *es = getenv("PGPB_CTC_SEGMENT");
-  if (es) TS = std::max(1, std::min(TS, atoi(es)));
+  if (tun.ctc_segment) TS = std::max(1, std::min(TS, tun.ctc_segment));
   while (TS > 64 && smem_bytes(Vp, Vw, W, TS, a.use_boost, nullptr, nullptr) > size_t(kSmemBudget)) TS -= 32;
   const size_t smem = smem_bytes(Vp, Vw, W, TS, a.use_boost, nullptr, nullptr);
   if (smem > 227 * 1024) {
@@ -1615,10 +1602,7 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
     return fail(PGPB_EINVAL, "vocabulary too large for the CTC walker's shared-memory root row");
   }
   a.TS = TS;
-  const char *ex = getenv("PGPB_CTC_STOP");
-  a.stop = ex ? atoi(ex) : 0;
-  const char *eq = getenv("PGPB_CTC_SEQ");
-  a.seq_mode = eq ? std::max(0, std::min(2, atoi(eq))) : 0;
+  a.seq_mode = std::max(0, std::min(2, tun.ctc_seq));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void *>(ctc_walk_kernel),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -1631,8 +1615,6 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctc_walk_kernel, 32 * (W + 1), smem);
   const int64_t cap = int64_t(sm_count(current_device())) * std::max(per_sm, 1);
   unsigned grid = unsigned(B < cap ? B : cap);
-  const char *eg = getenv("PGPB_CTC_GRID");  // timing experiments: cap the walker grid
-  if (eg && atoi(eg) > 0) grid = std::min(grid, unsigned(atoi(eg)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(32 * (W + 1));
@@ -1641,9 +1623,8 @@ int ctc_spec_launch(const pgpb_table *table, const float *d_lp, int64_t B, int64
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  const char *epdl = getenv("PGPB_CTC_PDL");
   cfg.attrs = attr;
-  cfg.numAttrs = (epdl && atoi(epdl) == 0) ? 0 : 1;
+  cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, ctc_walk_kernel, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (top) cudaFreeAsync(top, st);

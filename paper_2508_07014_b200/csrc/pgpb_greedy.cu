@@ -380,6 +380,15 @@ __global__ void __launch_bounds__(kThreads)
 
 }  // namespace pgpb
 
+namespace pgpb {
+// eos bump's final part (decoding.py:546-552): final_score[s] on final
+// states (clo_rec.w = is_final), 0 elsewhere.
+__global__ void final_bonus_kernel(TableView t, float *__restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < t.num_states) out[s] = __ldg(&t.clo_rec[s].w) ? __ldg(t.final_score + s) : 0.0f;
+}
+}  // namespace pgpb
+
 extern "C" {
 
 int pgpb_greedy_step(const pgpb_table *table, const float *d_lp, int64_t ld, int64_t R, int32_t V,
@@ -450,13 +459,12 @@ static int label_loop_launch(const pgpb_table *table, const float *d_lp, int64_t
   if (rc) return rc;
   // Warps per CTA: one row per warp is latency-bound, so spread the rows
   // over more SMs (fewer warps sharing an SM's schedulers) while the batch
-  // is small next to the GPU.  PGPB_LL_WARPS overrides (timing experiments).
+  // is small next to the GPU.  pgpb_set_tuning("ll.warps") overrides.
   int wpb = kWarpsPerBlock;
   {
-    const char *ew = getenv("PGPB_LL_WARPS");
     const int64_t nsm = sm_count(current_device());
-    if (ew) {
-      wpb = std::max(1, std::min(kWarpsPerBlock, atoi(ew)));
+    if (tuning().ll_warps) {
+      wpb = std::max(1, std::min(kWarpsPerBlock, tuning().ll_warps));
     } else {
       while (wpb > 2 && (R + wpb / 2 - 1) / (wpb / 2) <= nsm) wpb /= 2;
     }
@@ -465,6 +473,15 @@ static int label_loop_launch(const pgpb_table *table, const float *d_lp, int64_t
   fn<<<grid, 32 * wpb, smem, static_cast<cudaStream_t>(stream)>>>(
       t, use_boost ? 1 : 0, d_lp, ld, R, V, blank, lam, *state, d_emit, d_feed, d_any_active,
       static_cast<const __nv_bfloat16 *>(d_logits), ld_logits);
+  PGPB_CUDA_TRY(cudaGetLastError());
+  return PGPB_OK;
+}
+
+int pgpb_final_bonus(const pgpb_table *table, float *d_out, void *stream) {
+  using namespace pgpb;
+  if (!table || !d_out) return fail(PGPB_EINVAL, "NULL argument");
+  const TableView &t = table->view;
+  final_bonus_kernel<<<unsigned((t.num_states + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(t, d_out);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }

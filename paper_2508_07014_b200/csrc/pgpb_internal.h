@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+#include <exception>
+#include <new>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -9,6 +11,17 @@
 #include "pgpb.h"
 
 namespace pgpb {
+
+// Code-path overrides for tests (pgpb_set_tuning): 0 = automatic choice.
+// Every override selects between equivalent, bit-exact code paths; none
+// changes results.  Read on the host at launch time (no getenv).
+struct Tuning {
+  int ctc_consumers = 0;  // walker warps per CTA (1..7)
+  int ctc_segment = 0;    // frames per walker segment
+  int ctc_seq = 0;        // 1 = sequential walk, 2 = speculative rounds only
+  int ll_warps = 0;       // label-loop step: warps (rows) per CTA
+};
+Tuning &tuning();
 
 // Thread-local last-error message (pgpb_last_error).
 void set_error(const std::string &msg);
@@ -62,6 +75,24 @@ struct pgpb_table {
   int64_t closure_entries = 0;
   int32_t max_closure = 0;
 };
+
+// Host exceptions (std::bad_alloc from sizing vectors on untrusted input,
+// std::length_error, ...) must not cross the C ABI: every entry point that
+// allocates host containers runs its body through pgpb::guarded.
+namespace pgpb {
+template <typename F>
+int guarded(F &&body) {
+  try {
+    return body();
+  } catch (const std::bad_alloc &) {
+    return fail(PGPB_ENOMEM, "host allocation failed");
+  } catch (const std::exception &ex) {
+    return fail(PGPB_EINVAL, std::string("internal error: ") + ex.what());
+  } catch (...) {
+    return fail(PGPB_EINVAL, "internal error");
+  }
+}
+}  // namespace pgpb
 
 #define PGPB_CUDA_TRY(expr)                                                           \
   do {                                                                                \

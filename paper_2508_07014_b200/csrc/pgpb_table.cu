@@ -28,11 +28,16 @@ inline int32_t f2i(float f) {
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
+// Largest vocabulary a device table accepts: the dense root row (8 B per
+// token) is staged per CTA or read per row by every kernel; 2^26 tokens is
+// far beyond any tokenizer and keeps every size computation inside int32.
+constexpr int32_t kMaxVocab = 1 << 26;
+
 }  // namespace
 
 extern "C" {
 
-int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
+static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
                       const int32_t *arc_to, const float *arc_weight,
                       const int32_t *state_start, const int32_t *state_end,
                       const int32_t *backoff_to, const float *backoff_weight,
@@ -43,6 +48,9 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   *out = nullptr;
   if (S < 1 || V < 1) return fail(PGPB_EFORMAT, "need at least 1 state and 1 token");
   if (A < 0) return fail(PGPB_EFORMAT, "negative arc count");
+  if (V > kMaxVocab)
+    return fail(PGPB_EFORMAT, "vocab_size " + std::to_string(V) + " exceeds the device table limit " +
+                                  std::to_string(kMaxVocab));
   // Structural checks the kernels rely on (subset of table.py:87-127).
   for (int32_t s = 0; s < S; ++s) {
     if (state_start[s] < 0 || state_start[s] > state_end[s] || state_end[s] > A)
@@ -250,6 +258,15 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
   return PGPB_OK;
 }
 
+int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
+                      const int32_t *arc_to, const float *arc_weight,
+                      const int32_t *state_start, const int32_t *state_end,
+                      const int32_t *backoff_to, const float *backoff_weight,
+                      const uint8_t *is_final, const float *final_score, float unk_score,
+                      int32_t device, pgpb_table **out) {
+  return pgpb::guarded([&] { return pgpb_table_create_impl(S, V, A, arc_token, arc_to, arc_weight, state_start, state_end, backoff_to, backoff_weight, is_final, final_score, unk_score, device, out); });
+}
+
 // GPB1 (table.py:16-29 of the reference; little-endian): header
 // "<4sIIIIf" = magic, version=1, S, V, A, unk_score, then arc_from,
 // arc_token, arc_to (i32[A]), arc_weight (f32[A]), state_start, state_end,
@@ -257,7 +274,7 @@ int pgpb_table_create(int32_t S, int32_t V, int32_t A, const int32_t *arc_token,
 // final_score (f32[S]).  Parsed and validated on the host (the reference's
 // ArcTable.validate invariants, table.py:87-127), then the device arena is
 // built directly: no intermediate Python arrays.
-int pgpb_table_load_gpb1(const void *data, int64_t size, int32_t device, pgpb_table **out) {
+static int pgpb_table_load_gpb1_impl(const void *data, int64_t size, int32_t device, pgpb_table **out) {
   using pgpb::fail;
   if (!out) return fail(PGPB_EINVAL, "out is NULL");
   *out = nullptr;
@@ -276,6 +293,9 @@ int pgpb_table_load_gpb1(const void *data, int64_t size, int32_t device, pgpb_ta
   if (version != 1) return fail(PGPB_EFORMAT, "unsupported version " + std::to_string(version));
   if (S > uint32_t(INT32_MAX) || V > uint32_t(INT32_MAX) || A > uint32_t(INT32_MAX))
     return fail(PGPB_EFORMAT, "counts exceed int32");
+  if (V > uint32_t(kMaxVocab))
+    return fail(PGPB_EFORMAT, "vocab_size " + std::to_string(V) + " exceeds the device table limit " +
+                                  std::to_string(kMaxVocab));
   const int64_t expected = hdr + int64_t(A) * 16 + int64_t(S) * 21;
   if (size != expected)
     return fail(PGPB_EFORMAT, "expected " + std::to_string(expected) + " bytes, found " + std::to_string(size));
@@ -297,37 +317,65 @@ int pgpb_table_load_gpb1(const void *data, int64_t size, int32_t device, pgpb_ta
   const std::vector<float> arc_weight = take_f32(A);
   const std::vector<int32_t> state_start = take_i32(S), state_end = take_i32(S), backoff_to = take_i32(S);
   const std::vector<float> backoff_weight = take_f32(S);
-  std::vector<uint8_t> is_final(static_cast<size_t>(S));
+  std::vector<uint8_t> is_final(static_cast<size_t>(S));  // normalised to 0/1 below
   if (S) std::memcpy(is_final.data(), b + off, S);
   off += S;
   const std::vector<float> final_score = take_f32(S);
-  // ArcTable.validate (table.py:87-127): shapes, ranges, sort order, arc
-  // ranges consistent with arc_from, the root's backoff, finals
-  if (S < 1) return fail(PGPB_EFORMAT, "need at least the root state");
-  for (uint32_t j = 0; j < A; ++j) {
-    if (arc_from[j] < 0 || uint32_t(arc_from[j]) >= S) return fail(PGPB_EFORMAT, "arc_from out of range");
-    if (arc_token[j] < 0 || uint32_t(arc_token[j]) >= V) return fail(PGPB_EFORMAT, "arc_token out of range");
-    if (arc_to[j] < 0 || uint32_t(arc_to[j]) >= S) return fail(PGPB_EFORMAT, "arc_to out of range");
-    if (!std::isfinite(arc_weight[j])) return fail(PGPB_EFORMAT, "non-finite arc weight");
-    if (j && (arc_from[j] < arc_from[j - 1] || (arc_from[j] == arc_from[j - 1] && arc_token[j] <= arc_token[j - 1])))
-      return fail(PGPB_EFORMAT, "arcs not strictly sorted by (from, token)");
+  // ArcTable.validate (table.py:87-127), in the reference's check order:
+  // ranges, sort order, backoff targets, per-state arc ranges, coverage,
+  // root backoff, finals' zero backoff, non-final backoffs <= 0, finiteness.
+  // is_final is any nonzero byte (astype(bool), table.py:300).
+  if (S < 1 || V < 1)
+    return fail(PGPB_EFORMAT, "need at least 1 state and 1 token, got S=" + std::to_string(S) + " V=" +
+                                  std::to_string(V));
+  for (uint8_t &f : is_final) f = f ? 1 : 0;
+  auto all_in = [&](const std::vector<int32_t> &a, uint32_t hi) {
+    for (int32_t x : a)
+      if (x < 0 || uint32_t(x) >= hi) return false;
+    return true;
+  };
+  if (A) {
+    if (!all_in(arc_from, S)) return fail(PGPB_EFORMAT, "arc_from out of range");
+    if (!all_in(arc_to, S)) return fail(PGPB_EFORMAT, "arc_to out of range");
+    if (!all_in(arc_token, V)) return fail(PGPB_EFORMAT, "arc_token out of range");
+    for (uint32_t j = 1; j < A; ++j)
+      if (int64_t(arc_from[j]) * V + arc_token[j] <= int64_t(arc_from[j - 1]) * V + arc_token[j - 1])
+        return fail(PGPB_EFORMAT, "arcs not strictly sorted by (from_state, token)");
   }
+  if (!all_in(backoff_to, S)) return fail(PGPB_EFORMAT, "backoff_to out of range");
+  int64_t covered = 0;
   for (uint32_t st = 0; st < S; ++st) {
-    if (state_start[st] < 0 || state_start[st] > state_end[st] || uint32_t(state_end[st]) > A)
-      return fail(PGPB_EFORMAT, "state " + std::to_string(st) + ": bad arc range");
-    for (int32_t j = state_start[st]; j < state_end[st]; ++j)
-      if (uint32_t(arc_from[j]) != st) return fail(PGPB_EFORMAT, "arc range inconsistent with arc_from");
-    if (is_final[st] > 1) return fail(PGPB_EFORMAT, "is_final must be 0/1");
-    if (!std::isfinite(backoff_weight[st]) || !std::isfinite(final_score[st]))
-      return fail(PGPB_EFORMAT, "non-finite state score");
+    const int32_t lo = state_start[st], hi = state_end[st];
+    if (!(0 <= lo && lo <= hi && uint32_t(hi) <= A))
+      return fail(PGPB_EFORMAT, "state " + std::to_string(st) + ": bad arc range [" + std::to_string(lo) + ", " +
+                                    std::to_string(hi) + ")");
+    for (int32_t j = lo; j < hi; ++j)
+      if (uint32_t(arc_from[j]) != st)
+        return fail(PGPB_EFORMAT, "state " + std::to_string(st) + ": arc range covers foreign arcs");
+    covered += int64_t(hi) - lo;
   }
+  if (covered != int64_t(A)) return fail(PGPB_EFORMAT, "arc ranges do not cover the arc array");
   if (backoff_to[0] != 0 || backoff_weight[0] != 0.0f) return fail(PGPB_EFORMAT, "root backoff must be (0, 0)");
+  for (uint32_t st = 0; st < S; ++st)
+    if (is_final[st] && backoff_weight[st] != 0.0f)
+      return fail(PGPB_EFORMAT, "final states must have zero backoff weight");
+  for (uint32_t st = 1; st < S; ++st)
+    if (!is_final[st] && !(backoff_weight[st] <= 0.0f))
+      return fail(PGPB_EFORMAT, "non-final backoff weights must be <= 0");
+  for (uint32_t j = 0; j < A; ++j)
+    if (!std::isfinite(arc_weight[j])) return fail(PGPB_EFORMAT, "non-finite weight");
+  for (uint32_t st = 0; st < S; ++st)
+    if (!std::isfinite(backoff_weight[st])) return fail(PGPB_EFORMAT, "non-finite weight");
   return pgpb_table_create(int32_t(S), int32_t(V), int32_t(A), arc_token.data(), arc_to.data(), arc_weight.data(),
                            state_start.data(), state_end.data(), backoff_to.data(), backoff_weight.data(),
                            is_final.data(), final_score.data(), unk, device, out);
 }
 
-int pgpb_table_load_gpb1_file(const char *path, int32_t device, pgpb_table **out) {
+int pgpb_table_load_gpb1(const void *data, int64_t size, int32_t device, pgpb_table **out) {
+  return pgpb::guarded([&] { return pgpb_table_load_gpb1_impl(data, size, device, out); });
+}
+
+static int pgpb_table_load_gpb1_file_impl(const char *path, int32_t device, pgpb_table **out) {
   using pgpb::fail;
   if (!path) return fail(PGPB_EINVAL, "path is NULL");
   FILE *f = std::fopen(path, "rb");
@@ -340,6 +388,10 @@ int pgpb_table_load_gpb1_file(const char *path, int32_t device, pgpb_table **out
   const int rc = pgpb_table_load_gpb1(buf.data(), int64_t(buf.size()), device, out);
   if (rc != PGPB_OK) pgpb::set_error(std::string(path) + ": " + pgpb_last_error());
   return rc;
+}
+
+int pgpb_table_load_gpb1_file(const char *path, int32_t device, pgpb_table **out) {
+  return pgpb::guarded([&] { return pgpb_table_load_gpb1_file_impl(path, device, out); });
 }
 
 int pgpb_table_info_get(const pgpb_table *t, pgpb_table_info *out) {

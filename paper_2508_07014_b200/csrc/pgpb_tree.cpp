@@ -18,6 +18,11 @@
 
 namespace pgpb {
 
+Tuning &tuning() {
+  static Tuning t;
+  return t;
+}
+
 static thread_local std::string g_last_error;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
@@ -43,7 +48,20 @@ const char *pgpb_last_error(void) { return pgpb::g_last_error.c_str(); }
 
 int pgpb_abi_version(void) { return PGPB_ABI_VERSION; }
 
-int pgpb_trie_build(const int32_t *tokens, const int64_t *offsets, int64_t n_phrases,
+int pgpb_set_tuning(const char *key, int32_t value) {
+  if (!key) return pgpb::fail(PGPB_EINVAL, "key is NULL");
+  pgpb::Tuning &t = pgpb::tuning();
+  const std::string k(key);
+  if (value < 0) return pgpb::fail(PGPB_EINVAL, "tuning values are >= 0 (0 = automatic)");
+  if (k == "ctc.consumers") t.ctc_consumers = value;
+  else if (k == "ctc.segment") t.ctc_segment = value;
+  else if (k == "ctc.seq") t.ctc_seq = value;
+  else if (k == "ll.warps") t.ll_warps = value;
+  else return pgpb::fail(PGPB_EINVAL, "unknown tuning key " + k);
+  return PGPB_OK;
+}
+
+static int pgpb_trie_build_impl(const int32_t *tokens, const int64_t *offsets, int64_t n_phrases,
                     int32_t vocab_size, double c0, double beta, int32_t weight_mode,
                     double uniform_final_bonus, int64_t capacity, int32_t *parent,
                     int32_t *depth, int32_t *in_token, uint8_t *is_final, double *arc_sc,
@@ -120,6 +138,14 @@ int pgpb_trie_build(const int32_t *tokens, const int64_t *offsets, int64_t n_phr
   return PGPB_OK;
 }
 
+int pgpb_trie_build(const int32_t *tokens, const int64_t *offsets, int64_t n_phrases,
+                    int32_t vocab_size, double c0, double beta, int32_t weight_mode,
+                    double uniform_final_bonus, int64_t capacity, int32_t *parent,
+                    int32_t *depth, int32_t *in_token, uint8_t *is_final, double *arc_sc,
+                    double *acc, int64_t *num_nodes, int64_t *bad_phrase, int64_t *bad_token) {
+  return pgpb::guarded([&] { return pgpb_trie_build_impl(tokens, offsets, n_phrases, vocab_size, c0, beta, weight_mode, uniform_final_bonus, capacity, parent, depth, in_token, is_final, arc_sc, acc, num_nodes, bad_phrase, bad_token); });
+}
+
 // Children of every node as CSR sorted by (parent, token).
 static void children_csr(int64_t n, const int32_t *parent, const int32_t *in_token,
                          std::vector<int32_t> &start, std::vector<int32_t> &kids) {
@@ -135,7 +161,7 @@ static void children_csr(int64_t n, const int32_t *parent, const int32_t *in_tok
   }
 }
 
-int pgpb_trie_fail_links(int64_t n, const int32_t *parent, const int32_t *in_token,
+static int pgpb_trie_fail_links_impl(int64_t n, const int32_t *parent, const int32_t *in_token,
                          int32_t vocab_size, int32_t *fail_out) {
   using pgpb::fail;
   if (n < 1) return fail(PGPB_EINVAL, "tree needs a root");
@@ -172,7 +198,12 @@ int pgpb_trie_fail_links(int64_t n, const int32_t *parent, const int32_t *in_tok
   return PGPB_OK;
 }
 
-int pgpb_trie_compile(int64_t n, const int32_t *parent, const int32_t *in_token,
+int pgpb_trie_fail_links(int64_t n, const int32_t *parent, const int32_t *in_token,
+                         int32_t vocab_size, int32_t *fail_out) {
+  return pgpb::guarded([&] { return pgpb_trie_fail_links_impl(n, parent, in_token, vocab_size, fail_out); });
+}
+
+static int pgpb_trie_compile_impl(int64_t n, const int32_t *parent, const int32_t *in_token,
                       const uint8_t *is_final, const double *arc_sc, const double *acc,
                       const int32_t *fail_in, int32_t *arc_from, int32_t *arc_token,
                       int32_t *arc_to, float *arc_weight, int32_t *state_start,
@@ -206,6 +237,15 @@ int pgpb_trie_compile(int64_t n, const int32_t *parent, const int32_t *in_token,
     final_score[s] = is_final[s] ? static_cast<float>(acc[s]) : 0.0f;
   }
   return PGPB_OK;
+}
+
+int pgpb_trie_compile(int64_t n, const int32_t *parent, const int32_t *in_token,
+                      const uint8_t *is_final, const double *arc_sc, const double *acc,
+                      const int32_t *fail_in, int32_t *arc_from, int32_t *arc_token,
+                      int32_t *arc_to, float *arc_weight, int32_t *state_start,
+                      int32_t *state_end, int32_t *backoff_to, float *backoff_weight,
+                      float *final_score) {
+  return pgpb::guarded([&] { return pgpb_trie_compile_impl(n, parent, in_token, is_final, arc_sc, acc, fail_in, arc_from, arc_token, arc_to, arc_weight, state_start, state_end, backoff_to, backoff_weight, final_score); });
 }
 
 }  // extern "C"

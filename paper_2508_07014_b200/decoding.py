@@ -195,6 +195,8 @@ def ctc_greedy_device(logprobs, lengths, table: ArcTable | None, cfg: DecodeConf
     """Batched fused greedy CTC on device tensors, no host synchronisation.
 
     logprobs: float32 CUDA tensor [B, T, V]; lengths: int32 CUDA tensor [B] or None.
+    Lengths are not validated here (no host synchronisation); the kernels
+    clamp them to [0, T], so a bad length never addresses another row.
     """
     torch = _torch()
     if logprobs.dim() != 3 or logprobs.dtype != torch.float32 or not logprobs.is_cuda:
@@ -234,6 +236,12 @@ def ctc_greedy_boosted_batch(logprobs, lengths=None, table: ArcTable | None = No
     lp = logprobs if isinstance(logprobs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(logprobs, np.float32))
     lp = lp.to(device="cuda", dtype=torch.float32)
     ln = None if lengths is None else torch.as_tensor(np.asarray(lengths) if not isinstance(lengths, torch.Tensor) else lengths)
+    if ln is not None:
+        if tuple(ln.shape) != (lp.shape[0],):
+            raise ValueError(f"lengths must have shape ({lp.shape[0]},), got {tuple(ln.shape)}")
+        lo, hi = (int(x) for x in torch.aminmax(ln.to(torch.int64))) if ln.numel() else (0, 0)
+        if lo < 0 or hi > lp.shape[1]:
+            raise ValueError(f"lengths must lie in [0, {lp.shape[1]}], got [{lo}, {hi}]")
     o = ctc_greedy_device(lp, ln, table, cfg, blank_id)
     n = o.num_out.cpu().numpy()
     tok, dl, st = o.tokens.cpu().numpy(), o.deltas.cpu().numpy(), o.states.cpu().numpy()
@@ -600,7 +608,10 @@ def aed_beam_boosted(step: StepModel, table: ArcTable | None = None, cfg: Decode
         return _aed_beam_unfused(step, table, cfg, max_len, vocab, want_trace)
     rank = _rank_key(lam)
     topk = _TopK(table, use, V, lam)
-    row_max = table.device_table().row_max().cpu().numpy() if use and cfg.eos_bump_enabled else None
+    row_max = final_bonus = None
+    if use and cfg.eos_bump_enabled:  # device arrays: works for ArcTable and DeviceTable alike
+        row_max = table.device_table().row_max().cpu().numpy()
+        final_bonus = table.device_table().final_bonus().cpu().numpy()
     beam = [Hypothesis((), 0.0, 0.0, 0)]
     while True:
         active = [h for h in beam if not h.ended and len(h.tokens) < max_len]
@@ -613,8 +624,7 @@ def aed_beam_boosted(step: StepModel, table: ArcTable | None = None, cfg: Decode
             if row_max is not None:
                 best = float(row_max[h.tree_state])
                 bump = best if best > 0.0 else 0.0
-                if bool(table.is_final[h.tree_state]):
-                    bump += float(table.final_score[h.tree_state])
+                bump += float(final_bonus[h.tree_state])  # 0 unless final (decoding.py:551-552)
             cands.append(Hypothesis(h.tokens, h.am_score + float(rows[i, eos]), h.boost_score + bump, h.tree_state,
                                     h.last_token, ended=True,
                                     trace=h.trace + (TraceStep(eos, bump, h.tree_state),) if want_trace else ()))

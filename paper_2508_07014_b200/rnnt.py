@@ -50,6 +50,16 @@ def _torch():
     return torch
 
 
+
+def _check_lengths(ln, B: int, T: int) -> None:
+    """Frame counts must lie in [0, T] (the kernels index frames by them)."""
+    if tuple(ln.shape) != (B,):
+        raise ValueError(f"lengths must have shape ({B},), got {tuple(ln.shape)}")
+    if B:
+        lo, hi = (int(x) for x in ln.long().aminmax())
+        if lo < 0 or hi > T:
+            raise ValueError(f"lengths must lie in [0, {T}], got [{lo}, {hi}]")
+
 class RNNTModel:
     """Random-init prediction network (Embedding + 1-layer LSTM) and joint.
 
@@ -251,6 +261,7 @@ class LabelLoopingDecoder:
         self.enc_proj[:, :T].copy_(enc_proj)
         ln = torch.as_tensor(lengths, device=self.dev).long() if lengths is not None else torch.full(
             (B,), T, device=self.dev, dtype=torch.int64)
+        _check_lengths(ln, B, T)
         self.lengths.copy_(ln)
         for x in (self.t, self.k, self.n, self.am, self.boost, self.tree, self.h, self.c):
             x.zero_()

@@ -55,12 +55,13 @@ class _DeviceTable:
         self.device = device
         self._keep = None
         self._row_max = None
+        self._final = None
         self._destroy = _lib.LIB.pgpb_table_destroy  # survives interpreter teardown
 
     @classmethod
     def _from_handle(cls, handle: int, device: int) -> "_DeviceTable":
         d = cls.__new__(cls)
-        d.handle, d.device, d._keep, d._row_max = handle, device, None, None
+        d.handle, d.device, d._keep, d._row_max, d._final = handle, device, None, None, None
         d._destroy = _lib.LIB.pgpb_table_destroy
         return d
 
@@ -78,6 +79,17 @@ class _DeviceTable:
             _lib.check(_lib.LIB.pgpb_row_max(self.handle, out.data_ptr(), _lib.stream_ptr()))
             self._row_max = out
         return self._row_max
+
+    def final_bonus(self):
+        """final_score[s] on final states, 0 elsewhere, as a CUDA f32 tensor
+        (cached): the final part of the AED eos bump (decoding.py:546-552)."""
+        import torch
+
+        if self._final is None:
+            out = torch.empty(self.info().num_states, dtype=torch.float32, device=f"cuda:{self.device}")
+            _lib.check(_lib.LIB.pgpb_final_bonus(self.handle, out.data_ptr(), _lib.stream_ptr()))
+            self._final = out
+        return self._final
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -152,6 +164,14 @@ class ArcTable:
             s = int(bad[0])
             raise TableFormatError(f"state {s}: bad arc range [{int(lo[s])}, {int(hi[s])})")
         counts = hi - lo
+        if int(counts.sum()) > A:
+            # overlapping ranges: some state covers a foreign arc; find the
+            # first one as the reference's per-state loop does (table.py:113-117)
+            # without materialising every range (S x A for a hostile file)
+            for s in range(S):
+                if counts[s] and not (self.arc_from[lo[s]:hi[s]] == s).all():
+                    raise TableFormatError(f"state {s}: arc range covers foreign arcs")
+            raise TableFormatError("arc ranges do not cover the arc array")
         if A and counts.sum():
             owner = np.repeat(np.arange(S), counts)
             ends = np.cumsum(counts)

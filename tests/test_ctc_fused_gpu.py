@@ -1,4 +1,4 @@
-"""Fused speculative chunk-parallel greedy CTC (pgpb_ctc_fused.cu) vs the oracle.
+"""Fused speculative chunk-parallel greedy CTC (pgpb_ctc_spec.cu) vs the oracle.
 
 The fused kernel decides every chunk of frames from a guessed start and
 repairs the guesses in fix-up rounds; these tests drive the regimes that
@@ -10,8 +10,6 @@ and vocabularies that are not a multiple of 4 (scalar row loads).  Results
 must equal the reference restatement (oracle/pgpb_oracle.c, pinned to the
 reference's compiled kernel) bit for bit: tokens, am, boost and the trace.
 """
-
-import os
 
 import numpy as np
 import pytest
@@ -46,20 +44,17 @@ def _phrase_emissions(rng, phrases, T, V, noise=0.6, hit=4.0, blank_every=2):
 
 
 def _run(lps, lens, tab, lam, env=None):
-    from paper_2508_07014_b200 import DecodeConfig, ctc_greedy_boosted_batch
+    """Decode with the walker's code-path overrides (pgpb_set_tuning) set for
+    this call only; the keys name the walker's modes."""
+    from paper_2508_07014_b200 import DecodeConfig, _lib, ctc_greedy_boosted_batch
 
-    old = {}
     for k, v in (env or {}).items():
-        old[k] = os.environ.get(k)
-        os.environ[k] = v
+        _lib.set_tuning(k, int(v))
     try:
         return ctc_greedy_boosted_batch(lps, lens, tab, DecodeConfig(lam=lam), blank_id=0, want_trace=True)
     finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+        for k in (env or {}):
+            _lib.set_tuning(k, 0)
 
 
 def _check(got, lps, lens, tab, lam):
@@ -81,20 +76,20 @@ def t20k():
 @pytest.mark.parametrize("seq", ["0", "1", "2"])
 @pytest.mark.parametrize("lam", [0.0, 1.0, 2.5])
 def test_phrase_dense_deep_states(t20k, lam, seq):
-    """seq: PGPB_CTC_SEQ 0 = automatic mode choice, 1 = sequential walk,
+    """seq: ctc.seq 0 = automatic mode choice, 1 = sequential walk,
     2 = speculative rounds only."""
     phrases, V, tab = t20k
     rng = np.random.default_rng(31)
     B, T = 24, 400
     lps = np.stack([_phrase_emissions(rng, phrases, T, V) for _ in range(B)])
-    _check(_run(lps, None, tab, lam, {"PGPB_CTC_SEQ": seq}), lps, None, tab, lam)
+    _check(_run(lps, None, tab, lam, {"ctc.seq": seq}), lps, None, tab, lam)
 
 
-@pytest.mark.parametrize("env", [{"PGPB_CTC_CONSUMERS": "1"}, {"PGPB_CTC_CONSUMERS": "2"},
-                                 {"PGPB_CTC_CONSUMERS": "4"}, {"PGPB_CTC_SEGMENT": "97"},
-                                 {"PGPB_CTC_SEGMENT": "300", "PGPB_CTC_CONSUMERS": "3"},
-                                 {"PGPB_CTC_SEGMENT": "200", "PGPB_CTC_SEQ": "1"},
-                                 {"PGPB_CTC_SEGMENT": "111", "PGPB_CTC_SEQ": "2", "PGPB_CTC_CONSUMERS": "1"}])
+@pytest.mark.parametrize("env", [{"ctc.consumers": "1"}, {"ctc.consumers": "2"},
+                                 {"ctc.consumers": "4"}, {"ctc.segment": "97"},
+                                 {"ctc.segment": "300", "ctc.consumers": "3"},
+                                 {"ctc.segment": "200", "ctc.seq": "1"},
+                                 {"ctc.segment": "111", "ctc.seq": "2", "ctc.consumers": "1"}])
 def test_segments_and_consumer_counts(t20k, env):
     phrases, V, tab = t20k
     rng = np.random.default_rng(32)
@@ -131,7 +126,7 @@ def test_bench_regimes_vs_oracle(t20k, regime, seq):
             logits[:, np.arange(T) % 4 != 0, 0] += 10.0
         lps = gi.log_softmax(logits).astype(np.float32)
     for lam in (0.0, 1.0):
-        _check(_run(lps, None, tab, lam, {"PGPB_CTC_SEQ": seq}), lps, None, tab, lam)
+        _check(_run(lps, None, tab, lam, {"ctc.seq": seq}), lps, None, tab, lam)
 
 
 def test_small_tree_unk_root_rows():
@@ -156,36 +151,6 @@ def test_vocab_not_multiple_of_four(V):
     lens = rng.integers(0, T + 1, size=B).astype(np.int32)
     for lam in (1.0, 4.0):
         _check(_run(lps, lens, tab, lam), lps, lens, tab, lam)
-
-
-def test_fused_equals_two_phase(t20k):
-    """Same device outputs as the two-phase kernels (PGPB_CTC_TWOPHASE=1)."""
-    import torch
-
-    from paper_2508_07014_b200 import DecodeConfig, ctc_greedy_device
-
-    phrases, V, tab = t20k
-    g = torch.Generator(device="cuda")
-    g.manual_seed(36)
-    B, T = 96, 250
-    lp = torch.log_softmax(torch.randn((B, T, V), generator=g, device="cuda") * 2.0, dim=-1)
-    lens = torch.randint(0, T + 1, (B,), generator=g, device="cuda", dtype=torch.int32)
-    for lam in (0.0, 0.5, 1.0, 2.0):
-        cfg = DecodeConfig(lam=lam)
-        a = ctc_greedy_device(lp, lens, tab, cfg, 0)
-        os.environ["PGPB_CTC_TWOPHASE"] = "1"
-        try:
-            b = ctc_greedy_device(lp, lens, tab, cfg, 0)
-        finally:
-            os.environ.pop("PGPB_CTC_TWOPHASE")
-        torch.cuda.synchronize()
-        assert torch.equal(a.num_out, b.num_out)
-        assert torch.equal(a.am, b.am) and torch.equal(a.boost, b.boost)
-        for i in range(B):
-            n = int(a.num_out[i])
-            assert torch.equal(a.tokens[i, :n], b.tokens[i, :n])
-            assert torch.equal(a.deltas[i, :n], b.deltas[i, :n])
-            assert torch.equal(a.states[i, :n], b.states[i, :n])
 
 
 def test_empty_and_single_frame_batches(t20k):
@@ -238,7 +203,7 @@ def test_vocab_4096_general_phase_a(seq):
     lps = np.stack([_phrase_emissions(rng, phrases, T, V) for _ in range(B)])
     lens = rng.integers(1, T + 1, size=B).astype(np.int32)
     for lam in (0.0, 1.0):
-        _check(_run(lps, lens, tab, lam, {"PGPB_CTC_SEQ": seq}), lps, lens, tab, lam)
+        _check(_run(lps, lens, tab, lam, {"ctc.seq": seq}), lps, lens, tab, lam)
 
 
 @pytest.mark.parametrize("V", [1024, 64, 4])
