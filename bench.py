@@ -607,25 +607,21 @@ def cpu_ctc_reference(lps, tab, B, T, budget_s=2.0):
 
 
 def bench_device_beams(dev, rank, world):
-    """Configs 3 and 4 as batched device-resident beam searches (beams.py):
-    config 3 = RNN-T beam 4, 5K-phrase tree, V=1024, batch 64 x 200 frames,
-    random-init stateless prediction net + joint (bf16 GEMMs), max 5 symbols
-    per frame, one pgpb_tbeam_wave launch per wave, a frame replayed as a CUDA
-    graph; config 4 = AED beam 4, 20K-phrase tree, V=4096, batch 64, max_len
-    48, random-init 4-layer transformer decoder (d=256, FF 1024), one
-    pgpb_aed_step launch per token step.  Boosted (lam=1) vs unboosted
-    (lam=0), device time of one whole batch decode."""
+    """Configs 3 and 4 as batched device-resident beam searches (beams.py;
+    workloads in tests/bench_workloads.py, shared with the bench-shape parity
+    tests): config 3 = RNN-T beam 4, 5K-phrase tree, V=1024, batch 64 x 200
+    frames, random-init stateless prediction net + joint (bf16 GEMMs), max 5
+    symbols per frame, one pgpb_tbeam_wave launch per wave, a frame replayed
+    as a CUDA graph; config 4 = AED beam 4, 20K-phrase tree, V=4096, batch
+    64, max_len 48, random-init 4-layer transformer decoder (d=256, FF 1024)
+    with an eos logit offset (-4 + 0.4 * position) so hypotheses end inside
+    max_len, one pgpb_aed_step launch per token step.  Boosted (lam=1) vs
+    unboosted (lam=0), device time of one whole batch decode."""
     import torch
 
-    import gen_inputs as gi
+    import bench_workloads as bw
     import paper_2508_07014_b200 as pb
-    from paper_2508_07014_b200.beams import (AEDBeamDecoder, StatelessTransducerModel, TransducerBeamDecoder,
-                                             TransformerAEDModel)
-
-    def table(name):
-        phrases, V = gi.corpus(name)
-        ctx = pb.ContextList([pb.Phrase(" ".join(map(str, p)), p) for p in phrases], min_chars=0)
-        return pb.compile_arc_table(pb.compute_fail_links(pb.build_prefix_tree(ctx, pb.TreeParams(), V))), V
+    from paper_2508_07014_b200.beams import AEDBeamDecoder, TransducerBeamDecoder
 
     def timed(fn, n=3):
         fn()
@@ -642,16 +638,14 @@ def bench_device_beams(dev, rank, world):
 
     out = {}
     launches = 0
-    tab5, V = table("p5k_v1024")
-    B, T, D = 64, 200, 512
-    model = StatelessTransducerModel(V, enc_dim=D, pred_dim=640, joint_dim=640, seed=3 + rank, blank_bias=4.0)
-    g = torch.Generator(device=dev)
-    g.manual_seed(77 + rank)
-    enc = model.project_encoder(torch.randn((B, T, D), generator=g, device=dev))
+    c = bw.C3
+    model, tab5, enc = bw.config3(dev, rank)
+    B, T, V = c["B"], c["T"], tab5.vocab_size
     res = {"workload": f"RNN-T beam 4, batch {B} x {T} frames, V={V}, 5K-phrase tree, stateless pred net + joint, "
                        "max 5 symbols/frame"}
     for name, lam in (("unboosted", 0.0), ("boosted", 1.0)):
-        dec = TransducerBeamDecoder(model, tab5, pb.DecodeConfig(lam=lam, beam_size=4, max_symbols_per_frame=5), B, T)
+        dec = TransducerBeamDecoder(model, tab5, pb.DecodeConfig(lam=lam, beam_size=c["beam"],
+                                                                 max_symbols_per_frame=c["cap"]), B, T)
         ms = timed(lambda: dec.run(enc))
         launches += 4 * dec.launches
         best = dec.results()
@@ -660,15 +654,14 @@ def bench_device_beams(dev, rank, world):
     res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
     out["config3_rnnt_beam"] = res
     del dec, model, enc
-    tab20, V4 = table("p20k_v4096")
-    B, Tm, max_len = 64, 100, 48
-    model = TransformerAEDModel(V4, d_model=256, n_layers=4, n_heads=4, d_ff=1024, max_len=max_len + 1,
-                                seed=5 + rank)
-    mem = torch.randn((B, Tm, 256), generator=g, device=dev)
+    c = bw.C4
+    model, tab20, mem = bw.config4(dev, rank)
+    B, max_len, V4 = c["B"], c["max_len"], tab20.vocab_size
     res = {"workload": f"AED beam 4, batch {B}, V={V4}, 20K-phrase tree, 4-layer transformer decoder d=256, "
-                       f"max_len {max_len}, eos bump on"}
+                       f"max_len {max_len}, eos bump on, eos logit offset {c['eos_bias']} + {c['eos_ramp']} x pos"}
     for name, lam in (("unboosted", 0.0), ("boosted", 1.0)):
-        dec = AEDBeamDecoder(model, tab20, pb.DecodeConfig(lam=lam, beam_size=4), B, max_len=max_len, eos=V4 - 1)
+        dec = AEDBeamDecoder(model, tab20, pb.DecodeConfig(lam=lam, beam_size=c["beam"]), B, max_len=max_len,
+                             eos=V4 - 1)
         ms = timed(lambda: dec.run(mem))
         launches += 4 * dec.launches
         best = dec.results()
@@ -680,20 +673,21 @@ def bench_device_beams(dev, rank, world):
     return out
 
 
-def bench_rnnt(tab, V, dev, rank, world, B=128, T=200, D=512):
+def bench_rnnt(tab, V, dev, rank, world):
     """Config 2: greedy RNN-T label-looping with GPU-PB, 20K-phrase tree, V=1024,
     batch 128 x 200 frames of synthetic encoder output, random-init
-    LSTM-640 prediction net + joint; boosted (lam=1) vs unboosted (lam=0).
-    Device time of one whole batch decode (graph replays + done-flag polls)."""
+    LSTM-640 prediction net + joint (tests/bench_workloads.py); boosted
+    (lam=1) vs unboosted (lam=0).  Device time of one whole batch decode
+    (graph replays + done-flag polls)."""
     import torch
 
+    import bench_workloads as bw
     import paper_2508_07014_b200 as pb
-    from paper_2508_07014_b200.rnnt import LabelLoopingDecoder, RNNTModel
+    from paper_2508_07014_b200.rnnt import LabelLoopingDecoder
 
-    model = RNNTModel(V, enc_dim=D, pred_dim=640, joint_dim=640, seed=11 + rank, blank_bias=10.5)
-    g = torch.Generator(device=dev)
-    g.manual_seed(4321 + rank)
-    enc_proj = model.project_encoder(torch.randn((B, T, D), generator=g, device=dev))
+    c = bw.C2
+    model, tab, enc_proj = bw.config2(dev, rank)
+    B, T, D = c["B"], c["T"], c["D"]
     res = {"workload": f"greedy RNN-T label looping, batch {B} x {T} frames, V={V}, 20K-phrase tree, "
                        "LSTM-640 pred net + joint (random init), lam=1 vs lam=0"}
     iters = {}
@@ -721,6 +715,8 @@ def bench_rnnt(tab, V, dev, rank, world, B=128, T=200, D=512):
         from paper_2508_07014_b200.parallel import all_gather_results
         from paper_2508_07014_b200.rnnt import transducer_greedy_label_looping
 
+        g = torch.Generator(device=dev)
+        g.manual_seed(999 + rank)
         local = transducer_greedy_label_looping(model, torch.randn((B, T, D), generator=g, device=dev), None, tab,
                                                 pb.DecodeConfig(lam=1.0), want_trace=True)
         dist.barrier()

@@ -333,7 +333,8 @@ class TransformerAEDModel:
     """
 
     def __init__(self, vocab_size: int, d_model: int = 256, n_layers: int = 4, n_heads: int = 4, d_ff: int = 1024,
-                 max_len: int = 64, seed: int = 0, device="cuda", dtype=None):
+                 max_len: int = 64, seed: int = 0, device="cuda", dtype=None, eos_id: int | None = None,
+                 eos_bias: float = 0.0, eos_ramp: float = 0.0):
         torch = _torch()
         g = torch.Generator(device="cpu")
         g.manual_seed(seed)
@@ -356,6 +357,9 @@ class TransformerAEDModel:
                 "w1": w(d_ff, d, fan_in=d), "w2": w(d, d_ff, fan_in=d_ff),
             })
         self.w_out = w(vocab_size, d, fan_in=d) * 3.0
+        # eos logit offset eos_bias + eos_ramp * pos: sets where synthetic
+        # hypotheses end (a random-init decoder otherwise never prefers eos)
+        self.eos_id, self.eos_bias, self.eos_ramp = eos_id, float(eos_bias), float(eos_ramp)
 
     @staticmethod
     def _norm(x):
@@ -412,8 +416,10 @@ class TransformerAEDModel:
             x = x + ax.transpose(1, 2).reshape(N, d) @ lyr["wo_x"].T
             y = self._norm(x)
             x = x + F.gelu(y @ lyr["w1"].T) @ lyr["w2"].T
-        logits = self._norm(x) @ self.w_out.T
-        return torch.log_softmax(logits.float(), dim=-1)
+        logits = (self._norm(x) @ self.w_out.T).float()
+        if self.eos_id is not None and (self.eos_bias or self.eos_ramp):
+            logits[:, self.eos_id] += self.eos_bias + self.eos_ramp * pos
+        return torch.log_softmax(logits, dim=-1)
 
     def reorder(self, index, upto: int):
         """Slot i takes the caches of slot index[i] (positions 0..upto)."""
