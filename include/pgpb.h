@@ -324,7 +324,8 @@ int pgpb_row_max(const pgpb_table *table, float *d_out, void *stream);
  *               base = alt_am[h] if v == alt_token[h] else am[h]
  *      boost' = boost[h] + (double)score[state[h], v]      (0 if !use_boost)
  *      key    = am' + lam * boost'      (fp64, unfused; decoding.py:323-327)
- * and the best `k` (<= 32) per group are returned ordered by key desc,
+ * and the best `k` (any k; top-k runs in exact passes of 32 winners) per group are returned
+ * ordered by key desc,
  * am' desc, then (h, v) ascending.  With skip_neg_inf, candidates whose am'
  * is -inf are dropped (decoding.py:303-304).  The [H,V] score matrix is
  * never materialised.  Outputs are [G, k]; unfilled slots get hyp = -1.
@@ -427,6 +428,39 @@ typedef struct pgpb_aed_state {
 int pgpb_aed_step(const pgpb_table *table, const float *d_logprobs, int64_t ld, int64_t batch,
                   int32_t vocab_size, double lam, int32_t use_boost, const pgpb_aed_state *state,
                   void *stream);
+
+/* ------------------------------------------------------------------------
+ * Batched boosted greedy AED: aed_beam_boosted (decoding.py:502-587, R10)
+ * at beam 1, one decoder step for all B utterances.  Per utterance the step
+ * keeps the best of the eos candidate (am + lp[eos], boost + bump with the
+ * eos bump of decoding.py:546-552 when row_max != NULL) and every token
+ * v != eos (am + lp[v], boost + score[tree, v]) under the reference's rank
+ * (key = am + lam*boost, then am, then the token tuple: eos first on exact
+ * ties, then lower v).  Utterances with ended[b] or len[b] >= max_len are
+ * left untouched.  Writes tokens[b*max_len + len], the trace step
+ * (deltas / states at b*(max_len+1) + len: score or bump, next state), and
+ * feed[b] = the token the decoder consumes next; sets *any_active = 1 when
+ * an utterance can still extend (the caller zeroes it before the step).    */
+typedef struct pgpb_aed_greedy_state {
+  int32_t *tree;            /* [B] tree state                                */
+  double *am;               /* [B]                                           */
+  double *boost;            /* [B]                                           */
+  int32_t *len;             /* [B] tokens so far (eos not counted)           */
+  uint8_t *ended;           /* [B] 1 after eos                               */
+  int64_t *feed;            /* [B] next decoder input token                  */
+  int32_t *tokens;          /* [B, max_len]                                  */
+  double *deltas;           /* [B, max_len + 1] trace boosts (eos: the bump) */
+  int32_t *states;          /* [B, max_len + 1] trace states                 */
+  const float *row_max;     /* [S] pgpb_row_max, NULL = no eos bump          */
+  const float *final_bonus; /* [S] pgpb_final_bonus (with row_max)           */
+  int32_t *any_active;
+  int32_t max_len;
+  int32_t eos;
+} pgpb_aed_greedy_state;
+
+int pgpb_aed_greedy_step(const pgpb_table *table, const float *d_logprobs, int64_t ld, int64_t batch,
+                         int32_t vocab_size, double lam, int32_t use_boost, const pgpb_aed_greedy_state *state,
+                         void *stream);
 
 #ifdef __cplusplus
 }

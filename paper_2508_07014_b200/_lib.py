@@ -78,6 +78,15 @@ class AedState(ctypes.Structure):
                 ("beam", c_int32), ("max_len", c_int32), ("eos", c_int32), ("eos_bump", c_int32)]
 
 
+class AedGreedyState(ctypes.Structure):
+    """pgpb_aed_greedy_state."""
+
+    _fields_ = [("tree", c_void_p), ("am", c_void_p), ("boost", c_void_p), ("len", c_void_p), ("ended", c_void_p),
+                ("feed", c_void_p), ("tokens", c_void_p), ("deltas", c_void_p), ("states", c_void_p),
+                ("row_max", c_void_p), ("final_bonus", c_void_p), ("any_active", c_void_p),
+                ("max_len", c_int32), ("eos", c_int32)]
+
+
 # name -> argtypes (all return int unless listed in _VOID / _OTHER)
 _P = c_void_p
 _SIGS = {
@@ -118,6 +127,8 @@ _SIGS = {
                         POINTER(TBeamState), c_void_p],
     "pgpb_phrase_hits": [c_void_p, _P, _P, c_int64, _P, _P, _P, _P, _P, _P, c_void_p],
     "pgpb_aed_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_double, c_int32, POINTER(AedState), c_void_p],
+    "pgpb_aed_greedy_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_double, c_int32, POINTER(AedGreedyState),
+                             c_void_p],
 }
 
 # Every symbol include/pgpb.h declares (checked by tests/test_abi.py).

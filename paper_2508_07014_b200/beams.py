@@ -514,3 +514,113 @@ class AEDBeamDecoder:
     def decode(self, memory, *, record: bool = False, vocab=None, want_trace: bool = False) -> BeamOutput:
         records = self.run(memory, record=record)
         return BeamOutput(self.results(vocab, want_trace), records)
+
+
+class AEDGreedyDecoder:
+    """Batched boosted greedy AED (aed_beam_boosted at beam 1, R10): per step
+    one decoder step for the B utterances (TransformerAEDModel with one slot
+    each) and one pgpb_aed_greedy_step launch that fuses the argmax, the
+    boosted rerank and the eos bump.  Each step position
+    is captured as a CUDA graph on the second run and replayed afterwards."""
+
+    def __init__(self, model: TransformerAEDModel, table: ArcTable | None, cfg: DecodeConfig, batch: int, *,
+                 max_len: int, eos: int, device=None, poll: int = 4, use_graph: bool = True):
+        torch = _torch()
+        self.torch, self.model, self.table, self.cfg = torch, model, table, cfg
+        if table is not None and table.vocab_size != model.V:
+            raise ValueError(f"step model vocab size {model.V} != table vocab size {table.vocab_size}")
+        if max_len < 1:
+            raise ValueError(f"max_len must be >= 1, got {max_len}")
+        if max_len > model.max_len:
+            raise ValueError("max_len exceeds the model's positional table")
+        self.B, self.V, self.max_len, self.eos, self.poll = batch, model.V, max_len, eos, poll
+        self.use = _boost_active(table, cfg)
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.handle = table.device_table(self.dev.index).handle if self.use else None
+        bump = self.use and cfg.eos_bump_enabled
+        dt = table.device_table(self.dev.index) if bump else None
+        self._row_max = dt.row_max() if bump else None
+        self._final = dt.final_bonus() if bump else None
+        B, d = batch, self.dev
+        i32, i64, f64 = torch.int32, torch.int64, torch.float64
+        self.tree = torch.zeros(B, dtype=i32, device=d)
+        self.am = torch.zeros(B, dtype=f64, device=d)
+        self.boost = torch.zeros(B, dtype=f64, device=d)
+        self.len = torch.zeros(B, dtype=i32, device=d)
+        self.ended = torch.zeros(B, dtype=torch.uint8, device=d)
+        self.feed = torch.full((B,), model.V, dtype=i64, device=d)
+        self.tokens = torch.zeros((B, max_len), dtype=i32, device=d)
+        self.deltas = torch.zeros((B, max_len + 1), dtype=f64, device=d)
+        self.states = torch.zeros((B, max_len + 1), dtype=i32, device=d)
+        self.any_active = torch.zeros(1, dtype=i32, device=d)
+        self.flag_host = torch.zeros(1, dtype=i32, pin_memory=True)
+        p = lambda x: None if x is None else x.data_ptr()  # noqa: E731
+        self.state = _lib.AedGreedyState(p(self.tree), p(self.am), p(self.boost), p(self.len), p(self.ended),
+                                         p(self.feed), p(self.tokens), p(self.deltas), p(self.states),
+                                         p(self._row_max), p(self._final), p(self.any_active), max_len, eos)
+        self.launches = 0
+        self.use_graph, self._warm, self.graphs = use_graph, False, {}
+        self.pool = torch.cuda.graph_pool_handle() if use_graph else None
+
+    def _reset(self):
+        for x in (self.tree, self.am, self.boost, self.len, self.ended):
+            x.zero_()
+        self.feed.fill_(self.model.V)
+
+    def _step(self, n: int, records=None):
+        lp = self.model.step(self.feed, n)
+        if records is not None:
+            records.append((lp.cpu().numpy(), self.len.cpu().numpy().copy(), self.ended.cpu().numpy().copy()))
+        self.any_active.zero_()
+        _lib.check(_lib.LIB.pgpb_aed_greedy_step(self.handle, lp.data_ptr(), self.V, self.B, self.V,
+                                                 float(self.cfg.lam), int(self.use), _lib.ctypes.byref(self.state),
+                                                 _lib.stream_ptr()), "pgpb_aed_greedy_step")
+
+    def run(self, memory, *, record: bool = False):
+        torch, m = self.torch, self.model
+        m.start(memory, 1)
+        self._reset()
+        records = [] if record else None
+        self.launches = 0
+        graphs = self.use_graph and not record and self._warm
+        for n in range(self.max_len):
+            if graphs:
+                g = self.graphs.get(n)
+                if g is None:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, pool=self.pool):
+                        self._step(n)
+                    self.graphs[n] = g
+                g.replay()
+            else:
+                self._step(n, records)
+            self.launches += 1
+            if (n + 1) % self.poll == 0 or n + 1 == self.max_len:
+                self.flag_host.copy_(self.any_active, non_blocking=True)
+                torch.cuda.current_stream(self.dev).synchronize()
+                if int(self.flag_host[0]) == 0:
+                    break
+        if not record:
+            self._warm = True
+        return records
+
+    def results(self, vocab=None, want_trace: bool = False) -> list[DecodeResult]:
+        n = self.len.cpu().numpy()
+        ended = self.ended.cpu().numpy()
+        tok, dl, st = self.tokens.cpu().numpy(), self.deltas.cpu().numpy(), self.states.cpu().numpy()
+        am, bo = self.am.cpu().numpy(), self.boost.cpu().numpy()
+        out = []
+        for b in range(self.B):
+            k = int(n[b])
+            tokens = [int(x) for x in tok[b, :k]]
+            trace = None
+            if want_trace:
+                trace = [TraceStep(int(tok[b, i]), float(dl[b, i]), int(st[b, i])) for i in range(k)]
+                if ended[b]:
+                    trace.append(TraceStep(self.eos, float(dl[b, k]), int(st[b, k])))
+            out.append(DecodeResult(tokens, _text(tokens, vocab), float(am[b]), float(bo[b]), trace))
+        return out
+
+    def decode(self, memory, *, record: bool = False, vocab=None, want_trace: bool = False):
+        records = self.run(memory, record=record)
+        return BeamOutput(self.results(vocab, want_trace), records)

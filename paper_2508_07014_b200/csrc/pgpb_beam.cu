@@ -9,7 +9,9 @@
 //      (h, v) candidate — dense tokens from the shared-memory root row
 //      shifted by the state's backoff total, closure tokens from the closure
 //      — keeping a register-resident sorted top-K list per thread;
-//   3. K rounds of block-wide argmax merge the per-thread lists;
+//   3. k rounds of block-wide argmax merge the per-thread lists, in passes
+//      of up to 32 winners (each pass rescans below the previous pass's
+//      last winner, so any k is exact);
 //   4. the winners' tree score / next state are resolved (binary search in
 //      the sorted closure) and written out.
 // Never materialises the [H,V] score matrix.  All score arithmetic is fp64,
@@ -90,116 +92,142 @@ __global__ void __launch_bounds__(kBeamThreads) beam_topk_kernel(BeamArgs a) {
   }
   __syncthreads();
 
-  Cand list[K];
+  // Top-k in passes of up to 32 winners: pass p keeps, per thread, the best
+  // K candidates strictly below the previous pass's last winner (`floor`;
+  // the order (key, am, cid) is total, cid = hl * V + v unique), so the
+  // passes enumerate the exact global order for any k.
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int k = a.k;
+  bool have_floor = false;
+  Cand floor{INFINITY, INFINITY, -1};
+  for (int p0 = 0; p0 < k; p0 += kMaxTopK) {
+    const int rounds = min(kMaxTopK, k - p0);
+    Cand list[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+    for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
 
-  for (int hl = 0; hl < nh; ++hl) {
-    const int64_t h = h0 + hl;
-    if (a.valid && !a.valid[h]) continue;
-    const float *row = a.lp + h * a.ld;
-    const double am_h = a.am[h], boost_h = a.boost[h];
-    const int ex = a.exclude ? a.exclude[h] : -1;
-    const int alt = a.alt_token ? a.alt_token[h] : -1;
-    const double alt_am = a.alt_am ? a.alt_am[h] : 0.0;
-    float acc = 0.0f;
-    int4 rec = make_int4(0, 0, 0, 0);
-    if (a.use_boost) {
-      rec = __ldg(t.clo_rec + a.states[h]);
-      acc = __int_as_float(rec.z);
-    }
-    const unsigned *hbm = bm + hl * bm_words;
-    auto consider = [&](int v, float x, float s) {
-      if (v == ex) return;
-      const double base = (v == alt) ? alt_am : am_h;
-      const double amv = __dadd_rn(base, static_cast<double>(x));
-      if (a.skip_neg_inf && amv == -INFINITY) return;
-      const double bv = __dadd_rn(boost_h, static_cast<double>(s));
-      Cand c{__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, hl * V + v};
-      list_insert<K>(list, c);
-    };
-    if (kVec) {
-      const float4 *row4 = reinterpret_cast<const float4 *>(row);
-      for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) {
-        const float4 x4 = __ldg(row4 + i);
-        const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+    for (int hl = 0; hl < nh; ++hl) {
+      const int64_t h = h0 + hl;
+      if (a.valid && !a.valid[h]) continue;
+      const float *row = a.lp + h * a.ld;
+      const double am_h = a.am[h], boost_h = a.boost[h];
+      const int ex = a.exclude ? a.exclude[h] : -1;
+      const int alt = a.alt_token ? a.alt_token[h] : -1;
+      const double alt_am = a.alt_am ? a.alt_am[h] : 0.0;
+      float acc = 0.0f;
+      int4 rec = make_int4(0, 0, 0, 0);
+      if (a.use_boost) {
+        rec = __ldg(t.clo_rec + a.states[h]);
+        acc = __int_as_float(rec.z);
+      }
+      const unsigned *hbm = bm + hl * bm_words;
+      auto consider = [&](int v, float x, float s) {
+        if (v == ex) return;
+        const double base = (v == alt) ? alt_am : am_h;
+        const double amv = __dadd_rn(base, static_cast<double>(x));
+        if (a.skip_neg_inf && amv == -INFINITY) return;
+        const double bv = __dadd_rn(boost_h, static_cast<double>(s));
+        Cand c{__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, hl * V + v};
+        if (have_floor && !cand_better(floor, c)) return;
+        list_insert<K>(list, c);
+      };
+      if (kVec) {
+        const float4 *row4 = reinterpret_cast<const float4 *>(row);
+        for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) {
+          const float4 x4 = __ldg(row4 + i);
+          const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int v = 4 * i + j;
+          for (int j = 0; j < 4; ++j) {
+            const int v = 4 * i + j;
+            if (a.use_boost) {
+              if ((hbm[v >> 5] >> (v & 31)) & 1u) continue;
+              consider(v, xs[j], acc + root[v]);
+            } else {
+              consider(v, xs[j], 0.0f);
+            }
+          }
+        }
+      } else {
+        for (int v = threadIdx.x; v < V; v += blockDim.x) {
+          const float x = __ldg(row + v);
           if (a.use_boost) {
             if ((hbm[v >> 5] >> (v & 31)) & 1u) continue;
-            consider(v, xs[j], acc + root[v]);
+            consider(v, x, acc + root[v]);
           } else {
-            consider(v, xs[j], 0.0f);
+            consider(v, x, 0.0f);
           }
         }
       }
-    } else {
-      for (int v = threadIdx.x; v < V; v += blockDim.x) {
-        const float x = __ldg(row + v);
-        if (a.use_boost) {
-          if ((hbm[v >> 5] >> (v & 31)) & 1u) continue;
-          consider(v, x, acc + root[v]);
-        } else {
-          consider(v, x, 0.0f);
+      if (a.use_boost) {
+        for (int i = threadIdx.x; i < rec.y; i += blockDim.x) {
+          const int4 e = __ldg(t.clo + rec.x + i);
+          consider(e.x, __ldg(row + e.x), __int_as_float(e.z));
         }
       }
     }
-    if (a.use_boost) {
-      for (int i = threadIdx.x; i < rec.y; i += blockDim.x) {
-        const int4 e = __ldg(t.clo + rec.x + i);
-        consider(e.x, __ldg(row + e.x), __int_as_float(e.z));
-      }
-    }
-  }
 
-  // Block merge: k rounds of argmax over the per-thread list heads.
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int k = a.k;
-  for (int r = 0; r < k; ++r) {
-    Cand best = list[0];
+    // Block merge: `rounds` rounds of argmax over the per-thread list heads.
+    for (int r = 0; r < rounds; ++r) {
+      Cand best = list[0];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const Cand oc = shfl_cand(best, o);
-      if (cand_better(oc, best)) best = oc;
+      for (int o = 16; o; o >>= 1) {
+        const Cand oc = shfl_cand(best, o);
+        if (cand_better(oc, best)) best = oc;
+      }
+      if (lane == 0) s_warp[wid] = best;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        Cand b = s_warp[0];
+        for (int w = 1; w < kBeamThreads / 32; ++w)
+          if (cand_better(s_warp[w], b)) b = s_warp[w];
+        s_win[r] = b.cid;
+        s_win_key[r] = b.key;
+        s_win_am[r] = b.am;
+      }
+      __syncthreads();
+      if (s_win[r] != INT_MAX && list[0].cid == s_win[r]) list_pop<K>(list);
     }
-    if (lane == 0) s_warp[wid] = best;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      Cand b = s_warp[0];
-      for (int w = 1; w < kBeamThreads / 32; ++w)
-        if (cand_better(s_warp[w], b)) b = s_warp[w];
-      s_win[r] = b.cid;
-      s_win_key[r] = b.key;
-      s_win_am[r] = b.am;
+    for (int r = threadIdx.x; r < rounds; r += blockDim.x) {
+      const int64_t o = g * k + p0 + r;
+      const int cid = s_win[r];
+      if (cid == INT_MAX) {
+        a.out_hyp[o] = -1;
+        a.out_token[o] = -1;
+        a.out_am[o] = -INFINITY;
+        a.out_boost[o] = 0.0;
+        a.out_next[o] = 0;
+        a.out_delta[o] = 0.0f;
+        continue;
+      }
+      const int hl = cid / V, v = cid % V;
+      const int64_t h = h0 + hl;
+      float s = 0.0f;
+      int nx = 0;
+      if (a.use_boost) resolve_cell(t, root, rnext, a.states[h], v, s, nx);
+      a.out_hyp[o] = static_cast<int32_t>(h);
+      a.out_token[o] = v;
+      a.out_am[o] = s_win_am[r];
+      a.out_boost[o] = __dadd_rn(a.boost[h], static_cast<double>(s));
+      a.out_next[o] = nx;
+      a.out_delta[o] = s;
     }
+    const int last = s_win[rounds - 1];
+    floor = Cand{s_win_key[rounds - 1], s_win_am[rounds - 1], last};
+    have_floor = true;
     __syncthreads();
-    if (s_win[r] != INT_MAX && list[0].cid == s_win[r]) list_pop<K>(list);
-  }
-  __syncthreads();
-  for (int r = threadIdx.x; r < k; r += blockDim.x) {
-    const int64_t o = g * k + r;
-    const int cid = s_win[r];
-    if (cid == INT_MAX) {
-      a.out_hyp[o] = -1;
-      a.out_token[o] = -1;
-      a.out_am[o] = -INFINITY;
-      a.out_boost[o] = 0.0;
-      a.out_next[o] = 0;
-      a.out_delta[o] = 0.0f;
-      continue;
+    if (last == INT_MAX) {  // fewer candidates than k: the rest stay empty
+      for (int r = p0 + rounds + threadIdx.x; r < k; r += blockDim.x) {
+        const int64_t o = g * k + r;
+        a.out_hyp[o] = -1;
+        a.out_token[o] = -1;
+        a.out_am[o] = -INFINITY;
+        a.out_boost[o] = 0.0;
+        a.out_next[o] = 0;
+        a.out_delta[o] = 0.0f;
+      }
+      break;
     }
-    const int hl = cid / V, v = cid % V;
-    const int64_t h = h0 + hl;
-    float s = 0.0f;
-    int nx = 0;
-    if (a.use_boost) resolve_cell(t, root, rnext, a.states[h], v, s, nx);
-    a.out_hyp[o] = static_cast<int32_t>(h);
-    a.out_token[o] = v;
-    a.out_am[o] = s_win_am[r];
-    a.out_boost[o] = __dadd_rn(a.boost[h], static_cast<double>(s));
-    a.out_next[o] = nx;
-    a.out_delta[o] = s;
   }
 }
 
@@ -228,7 +256,6 @@ extern "C" int pgpb_beam_topk(const pgpb_table *table, const float *d_lp, int64_
   using namespace pgpb;
   if (hyps < 0 || V < 1 || (ld != 0 && ld < V) || group < 1 || k < 1)
     return fail(PGPB_EINVAL, "bad shape");
-  if (k > kMaxTopK) return fail(PGPB_EINVAL, "k must be <= 32");
   if (int64_t(group) * V >= INT_MAX) return fail(PGPB_EINVAL, "group * V too large");
   if (use_boost && !table) return fail(PGPB_EINVAL, "use_boost requires a table");
   if (table && table->view.vocab_size != V)

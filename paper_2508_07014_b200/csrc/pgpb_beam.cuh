@@ -6,7 +6,7 @@
 namespace pgpb {
 
 constexpr int kBeamThreads = 256;
-constexpr int kMaxTopK = 32;
+constexpr int kMaxTopK = 32;  // winners per merge pass (and the device beams' beam cap)
 
 struct Cand {
   double key;

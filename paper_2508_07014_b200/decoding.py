@@ -15,8 +15,8 @@ What runs where:
   * ctc_beam_boosted / transducer_beam_boosted / aed_beam_boosted -> the
     fused expansion + top-k kernel (pgpb_beam_topk) for every V-wide step;
     only the O(beam) hypothesis bookkeeping (prefix merges, eos handling)
-    stays on the host.  Beams wider than 16 fall back to the unfused form:
-    GPU advance rows + host candidate loops.
+    stays on the host.  Any beam width: the kernel's top-k runs in exact
+    passes of 32 winners.
 There is no CPU scoring path: the advance/rerank always runs on the GPU.
 """
 
@@ -36,7 +36,6 @@ NEG_INF = float("-inf")
 DEFAULT_BEAM_CTC = 8
 DEFAULT_BEAM_TRANSDUCER = 8
 DEFAULT_BEAM_AED = 3
-MAX_FUSED_BEAM = 16  # pgpb_beam_topk returns <= 32 candidates (beam + merges)
 
 
 @dataclass(frozen=True)
@@ -337,6 +336,7 @@ class _TopK:
                  valid=None, skip_neg_inf=False):
         torch = self.torch
         H = len(am)
+        k = min(int(k), H * self.V)  # never more winners than candidates
         dev = rows_dev.device
 
         def t(x, dt):
@@ -407,8 +407,6 @@ def ctc_beam_boosted(em: EmissionMatrix, table: ArcTable | None = None, cfg: Dec
     """
     cfg = cfg or DecodeConfig()
     _check_ctc_inputs(em, table)
-    if cfg.beam_size > MAX_FUSED_BEAM:
-        return _ctc_beam_unfused(em, table, cfg, vocab, want_trace)
     use = _boost_active(table, cfg)
     blank, lam, beam = em.blank_id, cfg.lam, cfg.beam_size
     lp = em.logprobs
@@ -438,7 +436,7 @@ def ctc_beam_boosted(em: EmissionMatrix, table: ArcTable | None = None, cfg: Dec
                 pnb = _logaddexp(pnb, e.pnb + float(lp[t, p[-1]]))
             new[p] = _Prefix(tot[j] + lb, pnb, e.state, e.boost, e.trace)
         # extensions to new prefixes: fused kernel top-k
-        k = min(32, beam + len(items))
+        k = beam + len(items)
         cands = topk(lp_dev[t], 0, [e.state for _, e in items], tot, [e.boost for _, e in items],
                      [blank] * len(items), k, alt_token=lastv, alt_am=[e.pb for _, e in items],
                      skip_neg_inf=True)
@@ -455,48 +453,6 @@ def ctc_beam_boosted(em: EmissionMatrix, table: ArcTable | None = None, cfg: Dec
              for p, e in ranked]
     return nbest[0], nbest
 
-
-def _ctc_beam_unfused(em, table, cfg, vocab, want_trace):
-    """Wide beams: GPU advance rows for all live prefixes, host V loops."""
-    use = _boost_active(table, cfg)
-    blank, lam, beam, lp, V = em.blank_id, cfg.lam, cfg.beam_size, em.logprobs, em.vocab_size
-    entries: dict[tuple, _Prefix] = {(): _Prefix(0.0, NEG_INF, 0, 0.0, ())}
-    rank = _prefix_rank(lam)
-    for t in range(em.num_frames):
-        items = list(entries.items())
-        if use:
-            q = get_scores_batch(table, [e.state for _, e in items])
-        new: dict[tuple, _Prefix] = {}
-        for i, (p, e) in enumerate(items):
-            tot = _logaddexp(e.pb, e.pnb)
-            ne = new.get(p)
-            if ne is None:
-                ne = new[p] = _Prefix(NEG_INF, NEG_INF, e.state, e.boost, e.trace)
-            ne.pb = _logaddexp(ne.pb, tot + float(lp[t, blank]))
-            last = p[-1] if p else -1
-            for v in range(V):
-                if v == blank:
-                    continue
-                lv = float(lp[t, v])
-                if v == last:
-                    ne.pnb = _logaddexp(ne.pnb, e.pnb + lv)
-                    contrib = e.pb + lv
-                else:
-                    contrib = tot + lv
-                if contrib == NEG_INF:
-                    continue
-                np_ = p + (v,)
-                ch = new.get(np_)
-                if ch is None:
-                    d, nx = (float(q.scores[i, v]), int(q.next_states[i, v])) if use else (0.0, 0)
-                    ch = new[np_] = _Prefix(NEG_INF, NEG_INF, nx, e.boost + d,
-                                            e.trace + (TraceStep(v, d, nx),) if want_trace else ())
-                ch.pnb = _logaddexp(ch.pnb, contrib)
-        entries = dict(sorted(new.items(), key=rank)[:beam])
-    ranked = sorted(entries.items(), key=rank)[:beam]
-    nbest = [DecodeResult(list(p), _text(p, vocab), e.am, e.boost, list(e.trace) if want_trace else None)
-             for p, e in ranked]
-    return nbest[0], nbest
 
 
 # ---------------------------------------------------------------------------
@@ -517,8 +473,6 @@ def transducer_beam_boosted(step: StepModel, num_frames: int, blank_id: int, tab
     _check_step_inputs(step, FLAVOR_TRANSDUCER, table)
     use = _boost_active(table, cfg)
     lam, beam_size, cap, V = cfg.lam, cfg.beam_size, cfg.max_symbols_per_frame, step.vocab_size
-    if beam_size > 32:
-        return _transducer_beam_unfused(step, num_frames, blank_id, table, cfg, vocab, want_trace)
     rank = _rank_key(lam)
     topk = _TopK(table, use, V, lam)
     beam = [Hypothesis((), 0.0, 0.0, 0)]
@@ -551,38 +505,6 @@ def transducer_beam_boosted(step: StepModel, num_frames: int, blank_id: int, tab
     return nbest[0], nbest
 
 
-def _transducer_beam_unfused(step, num_frames, blank_id, table, cfg, vocab, want_trace):
-    use = _boost_active(table, cfg)
-    lam, V, cap = cfg.lam, step.vocab_size, cfg.max_symbols_per_frame
-    rank = _rank_key(lam)
-    beam = [Hypothesis((), 0.0, 0.0, 0)]
-    for t in range(num_frames):
-        active: dict = {}
-        for h in beam:
-            _keep_better(active, (h.tokens, 0), h, lam)
-        finished: dict = {}
-        while active:
-            waves = sorted(active.items(), key=lambda kv: rank(kv[1]))
-            if use:
-                q = get_scores_batch(table, [h.tree_state for _, h in waves])
-            nxt_active: dict = {}
-            for i, ((toks, k), h) in enumerate(waves):
-                row = step.logprobs(h.last_token, t)
-                _keep_better(finished, h.tokens, replace(h, am_score=h.am_score + float(row[blank_id])), lam)
-                if k >= cap:
-                    continue
-                for v in range(V):
-                    if v == blank_id:
-                        continue
-                    d, nx = (float(q.scores[i, v]), int(q.next_states[i, v])) if use else (0.0, 0)
-                    c = Hypothesis(toks + (v,), h.am_score + float(row[v]), h.boost_score + d, nx, v,
-                                   trace=h.trace + (TraceStep(v, d, nx),) if want_trace else ())
-                    _keep_better(nxt_active, (c.tokens, k + 1), c, lam)
-            active = dict(sorted(nxt_active.items(), key=lambda kv: rank(kv[1]))[: cfg.beam_size])
-        beam = sorted(finished.values(), key=rank)[: cfg.beam_size]
-    nbest = _results(beam, lam, cfg.beam_size, vocab, want_trace)
-    return nbest[0], nbest
-
 
 # ---------------------------------------------------------------------------
 # AED beam
@@ -604,8 +526,6 @@ def aed_beam_boosted(step: StepModel, table: ArcTable | None = None, cfg: Decode
         raise ValueError(f"max_len must be >= 1, got {max_len}")
     use = _boost_active(table, cfg)
     lam, eos, V, beam_size = cfg.lam, step.eos_id, step.vocab_size, cfg.beam_size
-    if beam_size > 32:
-        return _aed_beam_unfused(step, table, cfg, max_len, vocab, want_trace)
     rank = _rank_key(lam)
     topk = _TopK(table, use, V, lam)
     row_max = final_bonus = None
@@ -640,36 +560,3 @@ def aed_beam_boosted(step: StepModel, table: ArcTable | None = None, cfg: Decode
     return nbest[0], nbest
 
 
-def _aed_beam_unfused(step, table, cfg, max_len, vocab, want_trace):
-    use = _boost_active(table, cfg)
-    lam, eos, V = cfg.lam, step.eos_id, step.vocab_size
-    rank = _rank_key(lam)
-    beam = [Hypothesis((), 0.0, 0.0, 0)]
-    while True:
-        active = [h for h in beam if not h.ended and len(h.tokens) < max_len]
-        if not active:
-            break
-        cands = [h for h in beam if h.ended or len(h.tokens) >= max_len]
-        if use:
-            q = get_scores_batch(table, [h.tree_state for h in active])
-        for i, h in enumerate(active):
-            row = step.logprobs(h.tokens, len(h.tokens))
-            for v in range(V):
-                lv = float(row[v])
-                if v == eos:
-                    bump = 0.0
-                    if use and cfg.eos_bump_enabled:
-                        best = float(q.scores[i].max())
-                        bump = best if best > 0.0 else 0.0
-                        if bool(table.is_final[h.tree_state]):
-                            bump += float(table.final_score[h.tree_state])
-                    cands.append(Hypothesis(h.tokens, h.am_score + lv, h.boost_score + bump, h.tree_state,
-                                            h.last_token, ended=True,
-                                            trace=h.trace + (TraceStep(eos, bump, h.tree_state),) if want_trace else ()))
-                else:
-                    d, nx = (float(q.scores[i, v]), int(q.next_states[i, v])) if use else (0.0, 0)
-                    cands.append(Hypothesis(h.tokens + (v,), h.am_score + lv, h.boost_score + d, nx, v,
-                                            trace=h.trace + (TraceStep(v, d, nx),) if want_trace else ()))
-        beam = sorted(cands, key=rank)[: cfg.beam_size]
-    nbest = _results(beam, lam, cfg.beam_size, vocab, want_trace)
-    return nbest[0], nbest

@@ -89,7 +89,7 @@ def test_ctc_beam_large_tree_vs_oracle():
         _cmp(nbest, orc.ctc_beam(lp, 0, tab, 1.0, beam))
 
 
-def test_unfused_wide_beams_vs_oracle():
+def test_wide_beams_vs_oracle():
     from paper_2508_07014_b200 import DecodeConfig, EmissionMatrix, TableStepModel, aed_beam_boosted, \
         ctc_beam_boosted, transducer_beam_boosted
 
@@ -110,6 +110,34 @@ def test_unfused_wide_beams_vs_oracle():
     astep = lambda p, n: arows.get(",".join(map(str, p)), adef)  # noqa: E731
     _, nb = aed_beam_boosted(am, tab, DecodeConfig(lam=1.0, beam_size=40), max_len=3, want_trace=True)
     _cmp(nb, orc.aed_beam(astep, tab, 1.0, 40, 3, V - 1, V))
+
+
+@pytest.mark.parametrize("beam", [64, 100])
+def test_beam_64_and_wider_vs_oracle(beam):
+    """Beam 64 (and 100: k = 200 candidates, 7 top-k passes) through the fused
+    kernel on a 200-token vocabulary with a 300-phrase tree: n-best equal to
+    the reference restatement (decoding.py:232-587)."""
+    from paper_2508_07014_b200 import DecodeConfig, EmissionMatrix, TableStepModel, aed_beam_boosted, \
+        ctc_beam_boosted, transducer_beam_boosted
+
+    rng = np.random.default_rng(beam)
+    V = 200
+    tab = product_table(gi.phrase_corpus(rng, V, 300), V)
+    lp = gi.random_emissions(rng, 10, V)
+    _, nb = ctc_beam_boosted(EmissionMatrix(lp, blank_id=0), tab, DecodeConfig(lam=1.0, beam_size=beam),
+                             want_trace=True)
+    _cmp(nb, orc.ctc_beam(lp, 0, tab, 1.0, beam))
+    rows, default = gi.random_transducer_rows(rng, V)
+    m = TableStepModel(flavor="transducer", default_row=default, rows=rows)
+    step = lambda last, t: rows.get("" if last is None else str(int(last)), default)  # noqa: E731
+    _, nb = transducer_beam_boosted(m, 3, 0, tab, DecodeConfig(lam=1.0, beam_size=beam, max_symbols_per_frame=2),
+                                    want_trace=True)
+    _cmp(nb, orc.transducer_beam(step, 3, 0, tab, 1.0, beam, 2, V))
+    arows, adef = gi.random_aed_rows(rng, V)
+    am = TableStepModel(flavor="aed", default_row=adef, rows=arows, eos_id=V - 1)
+    astep = lambda p, n: arows.get(",".join(map(str, p)), adef)  # noqa: E731
+    _, nb = aed_beam_boosted(am, tab, DecodeConfig(lam=1.0, beam_size=beam), max_len=3, want_trace=True)
+    _cmp(nb, orc.aed_beam(astep, tab, 1.0, beam, 3, V - 1, V))
 
 
 def test_exhaustive_ctc_beam_lambda_zero():
