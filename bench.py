@@ -621,7 +621,7 @@ def bench_device_beams(dev, rank, world):
 
     import bench_workloads as bw
     import paper_2508_07014_b200 as pb
-    from paper_2508_07014_b200.beams import AEDBeamDecoder, TransducerBeamDecoder
+    from paper_2508_07014_b200.beams import AEDBeamDecoder, AEDGreedyDecoder, TransducerBeamDecoder
 
     def timed(fn, n=3):
         fn()
@@ -669,6 +669,17 @@ def bench_device_beams(dev, rank, world):
         res[name] = {"ms": ms, "utt_per_s": B / (ms / 1e3) * world, "steps": dec.launches, "best_len_mean": toks}
     res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
     out["config4_aed_beam"] = res
+    res = {"workload": f"AED greedy (beam 1), batch {B}, V={V4}, 20K-phrase tree, the config-4 decoder and inputs, "
+                       "eos bump on; one pgpb_aed_greedy_step per token step"}
+    for name, lam in (("unboosted", 0.0), ("boosted", 1.0)):
+        dec = AEDGreedyDecoder(model, tab20, pb.DecodeConfig(lam=lam, beam_size=1), B, max_len=max_len, eos=V4 - 1)
+        ms = timed(lambda: dec.run(mem))
+        launches += 4 * dec.launches
+        best = dec.results()
+        res[name] = {"ms": ms, "utt_per_s": B / (ms / 1e3) * world, "steps": dec.launches,
+                     "best_len_mean": float(np.mean([len(r.tokens) for r in best]))}
+    res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
+    out["config4_aed_greedy"] = res
     out["_launches"] = launches
     return out
 
