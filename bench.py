@@ -433,16 +433,16 @@ def _ctc_regimes(B, T, V, dev, rank):
         tgt = [int(x) for x in rng.integers(1, V, size=T // 4 + 1)]
         ems.append(synth_ctc_emissions(tgt, vocab, margin=0.5, seed=int(rng.integers(2**31)), boost_positions=[],
                                        blanks_between=3).logprobs[:T])
-    yield "clean", torch.from_numpy(np.stack(ems)).to(dev)
+    yield "clean", torch.from_numpy(np.stack(ems)).to(dev), None
     del ems
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     logits = torch.randn((B, T, V), generator=g, device=dev) * 2.0
     lp = torch.log_softmax(logits, dim=-1)
-    yield "dense", lp
+    yield "dense", lp, None
     del lp
     logits[:, torch.arange(T, device=dev) % 4 != 0, 0] += 10.0
-    yield "blank3", torch.log_softmax(logits, dim=-1)
+    yield "blank3", torch.log_softmax(logits, dim=-1), None
     del logits
     # the clean shape at 5x the utterance length (40 s): the walker's latency
     # is per utterance, phase A's bandwidth cost per frame
@@ -452,7 +452,20 @@ def _ctc_regimes(B, T, V, dev, rank):
         tgt = [int(x) for x in rng.integers(1, V, size=TL // 4 + 1)]
         ems.append(synth_ctc_emissions(tgt, vocab, margin=0.5, seed=int(rng.integers(2**31)), boost_positions=[],
                                        blanks_between=3).logprobs[:TL])
-    yield f"clean_T{TL}", torch.from_numpy(np.stack(ems)).to(dev)
+    yield f"clean_T{TL}", torch.from_numpy(np.stack(ems)).to(dev), None
+    del ems
+    # the reference's own decode-overhead corpus, exactly (test_acceptance.py:
+    # 314-378: 25 utterances of ~1800 frames, 30 min of audio), one ragged batch
+    import gen_inputs as gi
+
+    targets, seeds, _ = gi.reference_overhead_corpus()
+    ems = [synth_ctc_emissions(tg, vocab, margin=0.5, seed=sd, boost_positions=[], blanks_between=3).logprobs
+           for tg, sd in zip(targets, seeds)]
+    lens = np.array([e.shape[0] for e in ems], np.int32)
+    pad = np.zeros((len(ems), int(lens.max()), V), np.float32)
+    for i, e in enumerate(ems):
+        pad[i, :e.shape[0]] = e
+    yield "ref_corpus_25x1800", torch.from_numpy(pad).to(dev), torch.from_numpy(lens).to(dev)
 
 
 def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
@@ -465,16 +478,16 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
     out = {"workload": f"greedy CTC, batch {B} x {T} frames, V={V}, 20K-phrase tree, lam=1 vs lam=0",
            "headline_regime": "clean"}
     launches = 0
-    for regime, lp in _ctc_regimes(B, T, V, dev, rank):
+    for regime, lp, lens in _ctc_regimes(B, T, V, dev, rank):
         lp = lp.contiguous()
-        res = {}
+        res, outs_ = {}, {}
         for name, cfg in (("unboosted", pb.DecodeConfig(lam=0.0)), ("boosted", pb.DecodeConfig(lam=1.0))):
-            o = pb.ctc_greedy_device(lp, None, tab, cfg, 0)
+            o = pb.ctc_greedy_device(lp, lens, tab, cfg, 0)
             torch.cuda.synchronize(dev)
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr):
                 for _ in range(reps):
-                    pb.ctc_greedy_device(lp, None, tab, cfg, 0, out=o)
+                    pb.ctc_greedy_device(lp, lens, tab, cfg, 0, out=o)
             gr.replay()
             torch.cuda.synchronize(dev)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -484,14 +497,24 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
             torch.cuda.synchronize(dev)
             launches += 2 * reps
             ms = s.elapsed_time(e) / reps
-            Tr = lp.shape[1]
-            res[name] = {"ms": ms, "rtfx": B * Tr * FRAME_SEC / (ms / 1e3) * world,
-                         "hbm_gbs": B * Tr * V * 4 / (ms / 1e3) / 1e9}
+            frames = int(lens.sum()) if lens is not None else lp.shape[0] * lp.shape[1]
+            res[name] = {"ms": ms, "rtfx": frames * FRAME_SEC / (ms / 1e3) * world,
+                         "hbm_gbs": frames * V * 4 / (ms / 1e3) / 1e9}
+            outs_[name] = (o.num_out.clone(), o.tokens.clone())
             if name == "boosted":
                 res["emitted_per_utt"] = float(o.num_out.double().mean().item())
         res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
+        if regime.startswith(("clean", "ref_corpus")):  # boosting must not change clean outputs (:377-378)
+            (nb, tb), (nu, tu) = outs_["boosted"], outs_["unboosted"]
+            valid = torch.arange(tb.shape[1], device=tb.device).unsqueeze(0) < nb.unsqueeze(1)
+            res["boosted_equals_unboosted"] = bool(torch.equal(nb, nu) and torch.equal(tb[valid], tu[valid]))
         if rank == 0 and regime in ("clean", "dense"):
             res["cpu_reference"] = cpu_ctc_reference(lp[: min(B, 32)].cpu().numpy(), tab, B, T)
+        if rank == 0 and regime.startswith("ref_corpus"):
+            ln = lens.cpu().numpy()
+            res["cpu_reference"] = cpu_ctc_reference([x[:n] for x, n in zip(lp.cpu().numpy(), ln)], tab,
+                                                     len(ln), float(ln.mean()))
+
         out[regime] = res
         del lp
     out["_launches"] = launches

@@ -932,6 +932,23 @@ __device__ BCand warp_decide(const Ctx &x, unsigned *bm, const float *row, int o
 #ifdef PGPB_SEQ_PROFILE
 __device__ int g_cf_step;
 #endif
+// Blank and repeat frames from f on (no decision, no table access): record
+// them as walk_step would and return the first frame that needs a decision
+// (or fe).
+__device__ __forceinline__ int pass_through(const Ctx &x, int f, int fe, int off, int &last) {
+  const Smem &s = *x.s;
+  for (; f < fe; ++f) {
+    const int a = s.fa[f];
+    if (a != x.blank && a != last) break;
+    s.in_off[f] = off;
+    s.in_last[f] = last;
+    s.o_tok[f] = -1;
+    s.o_lp[f] = s.flpa[f];
+    last = a;
+  }
+  return f;
+}
+
 __device__ __forceinline__ void walk_step(const Ctx &x, unsigned *bm, bool has, int f, int &off, int &st,
                                           int &last) {
   const Smem &s = *x.s;
@@ -1344,15 +1361,23 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
 #ifdef PGPB_SEQ_PROFILE
         const long long t_r0 = clock64();
 #endif
-        for (int k = 0; k < L; ++k) {
-          const int f = cb + k;
+        // Emission-compacted: each lane runs through its blank / repeat
+        // frames on its own (shared-memory records only) and the warp steps
+        // together only at decisions, so round 0 costs one dependent round
+        // trip per emission of the busiest lane instead of one per frame
+        // (L frames per chunk, almost every frame emits in some lane).
+        for (int f = cb;;) {
+          if (live) f = pass_through(x, f, ce, off, last);
+          const bool has = live && f < ce;
+          if (!__any_sync(kFull, has)) break;
 #ifdef PGPB_SEQ_PROFILE
           {
-            const unsigned hm = __ballot_sync(kFull, live && f < ce);
+            const unsigned hm = __ballot_sync(kFull, has);
             if (lane == 0) CF_COUNT(1, __popc(hm));
           }
 #endif
-          walk_step(x, bm, live && f < ce, f, off, st, last);
+          walk_step(x, bm, has, f, off, st, last);
+          if (has) ++f;
         }
         s.c_eoff[c] = off;
         s.c_est[c] = st;

@@ -104,3 +104,27 @@ CORPORA = {
 def corpus(name: str):
     V, n = CORPORA[name]
     return phrase_corpus(np.random.default_rng(1008), V, n), V
+
+
+def reference_overhead_corpus():
+    """The reference's decode-overhead corpus (test_acceptance.py:314-355),
+    replaying its RNG call order exactly: default_rng(1008) -> the 20K and
+    200-phrase corpora (:320, :326), two query-state draws of (100, 32)
+    (:331-332, small table first), then 25 x (450 random targets, a seed)
+    for synth_ctc_emissions(margin=0.5, boost_positions=[], blanks_between=3)
+    (:342-353).  Returns (targets, seeds, S_small); the caller builds the
+    emissions with its synth_ctc_emissions (acoustic.py:133-200 semantics)."""
+    V = 1024
+    rng = np.random.default_rng(1008)
+    phrase_corpus(rng, V, 20_000)
+    small = phrase_corpus(rng, V, 200)
+    # the small table's state count: root + distinct prefixes (trie nodes)
+    prefixes = {p[:i] for p in small for i in range(1, len(p) + 1)}
+    s_small, s_big = 1 + len(prefixes), 140_870
+    rng.integers(0, s_small, size=(100, 32))
+    rng.integers(0, s_big, size=(100, 32))
+    targets, seeds = [], []
+    for _ in range(25):
+        targets.append([int(x) for x in rng.integers(1, V, size=450)])
+        seeds.append(int(rng.integers(2**31)))
+    return targets, seeds, s_small
