@@ -1211,7 +1211,14 @@ __global__ void __launch_bounds__(32 * (kMaxConsumers + 1), 1) ctc_walk_kernel(A
         int4 r[4];  // all loads in flight before the first store: one round trip
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (f0 + u * nthreads < n) r[u] = __ldg(top + f0 + u * nthreads);
+          if (f0 + u * nthreads < n) {
+            if (boost) {
+              r[u] = __ldg(top + f0 + u * nthreads);
+            } else {  // unboosted phase A writes only the {a, lp_a} half
+              const int2 h = __ldg(reinterpret_cast<const int2 *>(top + f0 + u * nthreads));
+              r[u] = make_int4(h.x, h.y, 0, 0);
+            }
+          }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int f = f0 + u * nthreads;

@@ -241,7 +241,12 @@ def ctc_greedy_boosted_batch(logprobs, lengths=None, table: ArcTable | None = No
         lo, hi = (int(x) for x in torch.aminmax(ln.to(torch.int64))) if ln.numel() else (0, 0)
         if lo < 0 or hi > lp.shape[1]:
             raise ValueError(f"lengths must lie in [0, {lp.shape[1]}], got [{lo}, {hi}]")
-    o = ctc_greedy_device(lp, ln, table, cfg, blank_id)
+    B, T = lp.shape[0], lp.shape[1]
+    z = lambda *shape, dt: torch.zeros(shape, dtype=dt, device=lp.device)  # noqa: E731
+    # zero-filled: the whole [B, T] arrays are copied back, slots past num_out included
+    o = ctc_greedy_device(lp, ln, table, cfg, blank_id, out=GreedyBatchOutput(
+        z(B, T, dt=torch.int32), z(B, T, dt=torch.float64), z(B, T, dt=torch.int32), z(B, dt=torch.int32),
+        z(B, dt=torch.float64), z(B, dt=torch.float64)))
     n = o.num_out.cpu().numpy()
     tok, dl, st = o.tokens.cpu().numpy(), o.deltas.cpu().numpy(), o.states.cpu().numpy()
     am, bo = o.am.cpu().numpy(), o.boost.cpu().numpy()
