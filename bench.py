@@ -291,6 +291,8 @@ def run_ours(args, rank, world, local):
         out["decode_beams"] = bench_beams()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(tab, TOTAL_STATES, V)
+        if not args.no_decode:
+            out["cpu_reference_decoders"] = bench_cpu_decoders(torch.device("cuda", local))
     if not args.no_decode:
         out["decode_summary"] = decode_summary(out)
     return out
@@ -825,6 +827,164 @@ def bench_beams(budget_s=6.0):
                        "hyps_per_s_cpu": 1 / c_s, "same_best": g_out == c_out}
     res["note"] = ("per-utterance calls of the reference-facing API (host StepModel rows, one fused "
                    "pgpb_beam_topk launch per step/wave); CPU = oracle port of the reference's Python beams, 1 thread")
+    return res
+
+
+def _reference_package():
+    """The reference's own Python package (baseline/_ref/pkg/src, copied by
+    __graft_entry__.build()) with its compiled kernel module from oracle/_ref
+    installed as the backend (the reference's compiled configuration), or
+    None when the copy is absent.  Used only by the CPU legs below."""
+    src = ROOT / "baseline" / "_ref" / "pkg" / "src"
+    if not (src / "phraseboost").is_dir():
+        return None
+    if str(src) not in sys.path:
+        sys.path.insert(0, str(src))
+    import phraseboost
+    import phraseboost._backend as be
+
+    mod, _ = _ref_module()
+    if mod is not None and be._kernels is None:
+        be._kernels = mod
+        be.HAVE_COMPILED = True
+    return phraseboost
+
+
+def bench_cpu_decoders(dev, budget_s=4.0):
+    """The reference's own decoders (decoding.py:350-587, pure Python over
+    its compiled kernels) on the host, fed the exact log-prob rows our GPU
+    decoders consumed at the config 2/3/4 bench shapes (recorded on the
+    device, replayed through the reference's StepModel contract,
+    acoustic.py:203-217), on a bounded sample of utterances: ms per
+    utterance, RTFx / utterances per s, and whether the reference's output
+    equals ours.  1 host thread (the reference decoders are GIL-bound)."""
+    import torch
+
+    import bench_workloads as bw
+    import paper_2508_07014_b200 as pb
+    from paper_2508_07014_b200.beams import AEDBeamDecoder, AEDGreedyDecoder, TransducerBeamDecoder, _walk
+    from paper_2508_07014_b200.rnnt import LabelLoopingDecoder
+
+    ref = _reference_package()
+    if ref is None:
+        return {"unavailable": "baseline/_ref/pkg not present (run __graft_entry__.build() where /root/reference exists)"}
+    from phraseboost import DecodeConfig as RCfg
+    from phraseboost.acoustic import StepModel as RStep
+
+    def rtable(corpus):
+        phrases, V = __import__("gen_inputs").corpus(corpus)
+        ctx = ref.ContextList(phrases=[ref.Phrase(" ".join(map(str, p)), tuple(p)) for p in phrases], min_chars=0)
+        return ref.compile_arc_table(ref.compute_fail_links(ref.build_prefix_tree(ctx, ref.TreeParams(), V))), V
+
+    class Replay(RStep):
+        def __init__(self, flavor, V, fn, eos=None):
+            self.flavor, self.vocab_size, self.eos_id, self.fn = flavor, V, eos, fn
+
+        def logprobs(self, context, step):
+            return self.fn(context, step)
+
+    def timed(fn, n_utts):
+        t0 = time.perf_counter()
+        outs = [fn(i) for i in range(n_utts)]
+        return (time.perf_counter() - t0) / n_utts, outs
+
+    res = {"kind": "reference", "cores": 1, "backend": ref._backend.backend_name(),
+           "impl": "baseline/_ref phraseboost decoders + oracle/_ref compiled _kernels",
+           "note": "rows recorded from the GPU decode of the bench inputs, replayed into the reference decoders"}
+    # ---- config 2: greedy RNN-T (transducer_greedy_boosted, decoding.py:350-393)
+    c = bw.C2
+    model, _, enc_proj = bw.config2(dev)
+    ptab = bw.table(c["corpus"])[0]
+    rt, V = rtable(c["corpus"])
+    dec = LabelLoopingDecoder(model, ptab, pb.DecodeConfig(lam=1.0), c["B"], c["T"], use_graph=False)
+    o = dec.decode(enc_proj, record=True)
+    n_ok = 0
+    n = 6
+
+    def one_greedy(b):
+        rows = iter([r[0][b] for r in o.records if r[1][b]])
+        st = Replay("transducer", V, lambda last, t: next(rows))
+        return ref.transducer_greedy_boosted(st, c["T"], 0, rt, RCfg(lam=1.0))
+
+    sec, outs = timed(one_greedy, n)
+    ntok = o.num_out.cpu().numpy()
+    toks = o.tokens.cpu().numpy()
+    n_ok = sum(list(r.tokens) == [int(x) for x in toks[b, :ntok[b]]] for b, r in enumerate(outs))
+    res["config2_rnnt_greedy"] = {"sample": f"{n} of {c['B']} utterances x {c['T']} frames", "ms_per_utt": sec * 1e3,
+                                  "rtfx": c["T"] * FRAME_SEC / sec, "same_tokens": f"{n_ok}/{n}"}
+    del dec, o
+    # ---- config 3: RNN-T beam 4 (transducer_beam_boosted, decoding.py:428-495), frames cut to 50
+    c = bw.C3
+    model, ptab_unused, enc = bw.config3(dev)
+    ptab = bw.table(c["corpus"])[0]
+    rt, V = rtable(c["corpus"])
+    T3 = 50
+    dec = TransducerBeamDecoder(model, ptab, pb.DecodeConfig(lam=1.0, beam_size=c["beam"],
+                                                             max_symbols_per_frame=c["cap"]), c["B"], c["T"],
+                                use_graph=False)
+    out = dec.decode(enc, torch.full((c["B"],), T3), record=True)
+
+    def one_tbeam(b):
+        rows = {}
+        for lp, flags, last, t in out.records:
+            if t[b] < T3:
+                for r in range(c["beam"]):
+                    if flags[b, r] & 1:
+                        rows[(int(last[b, r]), int(t[b]))] = lp[b, r]
+        st = Replay("transducer", V, lambda last, t: rows[(-1 if last is None else int(last), t)])
+        return ref.transducer_beam_boosted(st, T3, 0, rt, RCfg(lam=1.0, beam_size=c["beam"],
+                                                               max_symbols_per_frame=c["cap"]))[0]
+
+    n = 1
+    t0 = time.perf_counter()
+    outs = []
+    while len(outs) < 4 and (not outs or time.perf_counter() - t0 < budget_s):
+        outs.append(one_tbeam(len(outs)))
+    sec = (time.perf_counter() - t0) / len(outs)
+    n_ok = sum(list(r.tokens) == list(out.nbest[b][0].tokens) for b, r in enumerate(outs))
+    res["config3_rnnt_beam"] = {"sample": f"{len(outs)} of {c['B']} utterances x {T3} frames", "ms_per_utt": sec * 1e3,
+                                "rtfx": T3 * FRAME_SEC / sec, "same_best": f"{n_ok}/{len(outs)}"}
+    del dec, out
+    # ---- config 4: AED beam 4 and greedy (aed_beam_boosted, decoding.py:502-587)
+    c = bw.C4
+    model, ptab, mem = bw.config4(dev)
+    rt, V = rtable(c["corpus"])
+    eos = V - 1
+    for name, beam, Dec in (("config4_aed_beam", c["beam"], AEDBeamDecoder), ("config4_aed_greedy", 1, AEDGreedyDecoder)):
+        dec = Dec(model, ptab, pb.DecodeConfig(lam=1.0, beam_size=beam), c["B"], max_len=c["max_len"], eos=eos,
+                  use_graph=False, **({"poll": 1} if Dec is AEDBeamDecoder else {}))
+        out = dec.decode(mem, record=True)
+
+        def rows_of(b):
+            rows = {}
+            if Dec is AEDBeamDecoder:
+                for lp, hy, tr in out.records:
+                    for r in range(beam):
+                        f = int(hy["flags"][b, r])
+                        if (f & 1) and not (f & 2) and hy["len"][b, r] < c["max_len"]:
+                            rows[tuple(s_[0] for s_ in _walk(tr, b, int(hy["node"][b, r])))] = lp[b, r]
+            else:
+                toks = list(out.nbest[b].tokens)
+                for lp, ln, ended in out.records:
+                    if not ended[b] and ln[b] < c["max_len"]:
+                        rows[tuple(toks[:int(ln[b])])] = lp[b]
+            return rows
+
+        def one_aed(b):
+            rows = rows_of(b)
+            st = Replay("aed", V, lambda p, n_: rows[tuple(p)], eos=eos)
+            return ref.aed_beam_boosted(st, rt, RCfg(lam=1.0, beam_size=beam), max_len=c["max_len"])[0]
+
+        t0 = time.perf_counter()
+        outs = []
+        while len(outs) < 4 and (not outs or time.perf_counter() - t0 < budget_s):
+            outs.append(one_aed(len(outs)))
+        sec = (time.perf_counter() - t0) / len(outs)
+        ours = [out.nbest[b][0] if Dec is AEDBeamDecoder else out.nbest[b] for b in range(len(outs))]
+        n_ok = sum(list(r.tokens) == list(g.tokens) for r, g in zip(outs, ours))
+        res[name] = {"sample": f"{len(outs)} of {c['B']} utterances, max_len {c['max_len']}", "ms_per_utt": sec * 1e3,
+                     "utt_per_s": 1.0 / sec, "same_best": f"{n_ok}/{len(outs)}"}
+        del dec, out
     return res
 
 
