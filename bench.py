@@ -287,6 +287,8 @@ def run_ours(args, rank, world, local):
         out["gpu_launches"] += out["decode_ctc"].pop("_launches", 0)
         out["decode_device_beams"] = bench_device_beams(dev, rank, world)
         out["gpu_launches"] += out["decode_device_beams"].pop("_launches", 0)
+        out["decode_ctc_beam"] = bench_ctc_beam(tab, V, dev, rank, world)
+        out["gpu_launches"] += out["decode_ctc_beam"].pop("_launches", 0)
     if rank == 0 and world == 1 and not args.no_decode:
         out["decode_beams"] = bench_beams()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -310,6 +312,10 @@ def decode_summary(out):
         if isinstance(v, dict) and "overhead" in v:
             d[f"ctc_greedy_{k}"] = {"unboosted_ms": round(v["unboosted"]["ms"], 5),
                                     "boosted_ms": round(v["boosted"]["ms"], 5), "overhead": round(v["overhead"], 4)}
+    for k, v in out.get("decode_ctc_beam", {}).items():
+        if isinstance(v, dict) and "overhead" in v:
+            d[f"ctc_beam_{k}"] = {"unboosted_ms": round(v["unboosted"]["ms"], 4),
+                                  "boosted_ms": round(v["boosted"]["ms"], 4), "overhead": round(v["overhead"], 4)}
     for k, v in out.get("decode_device_beams", {}).items():
         if isinstance(v, dict) and "overhead" in v:
             d[k] = {"unboosted_ms": round(v["unboosted"]["ms"], 4), "boosted_ms": round(v["boosted"]["ms"], 4),
@@ -629,6 +635,51 @@ def cpu_ctc_reference(lps, tab, B, T, budget_s=2.0):
     return {"kind": kind, "sample": f"{len(utts)} utterances of the batch, repeated for ~{budget_s:.0f} s",
             "ms_per_batch_1thread": t1 * B * 1e3, "ms_per_batch": tn * B * 1e3, "cores": threads,
             "rtfx": T * FRAME_SEC / tn, "rtfx_1thread": T * FRAME_SEC / t1}
+
+
+def bench_ctc_beam(tab, V, dev, rank, world, B=64, T=200, beam=4):
+    """Batched device CTC prefix beam (pgpb_ctc_beam: one launch decodes every
+    frame of every utterance), 20K-phrase tree, beam 4, batch 64 x 200 frames:
+    the clean regime (synth_ctc_emissions, blanks_between=3) and random
+    log_softmax(N(0, 2)) rows; boosted (lam=1) vs unboosted (lam=0), device
+    time of one whole batch decode."""
+    import torch
+
+    import paper_2508_07014_b200 as pb
+    from paper_2508_07014_b200.beams import ctc_beam_batch, ctc_beam_device
+
+    out = {"workload": f"CTC prefix beam {beam}, batch {B} x {T} frames, V={V}, 20K-phrase tree, device resident"}
+    launches = 0
+    for regime, lp, _ in _ctc_regimes(B, T, V, dev, rank):
+        if regime not in ("clean", "dense"):
+            continue
+        lp = lp.contiguous()
+        res = {}
+        for name, lam in (("unboosted", 0.0), ("boosted", 1.0)):
+            cfg = pb.DecodeConfig(lam=lam, beam_size=beam)
+            ctc_beam_device(lp, None, tab, cfg, 0)
+            ts = []
+            for _ in range(3):
+                torch.cuda.synchronize(dev)
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                ctc_beam_device(lp, None, tab, cfg, 0)
+                e.record()
+                torch.cuda.synchronize(dev)
+                ts.append(s.elapsed_time(e))
+                launches += 1
+            ms = statistics.median(ts)
+            t0 = time.perf_counter()
+            r = ctc_beam_batch(lp, None, tab, cfg, blank_id=0)
+            e2e = (time.perf_counter() - t0) * 1e3
+            res[name] = {"ms": ms, "rtfx": B * T * FRAME_SEC / (ms / 1e3) * world, "e2e_ms": e2e,
+                         "best_len_mean": float(np.mean([len(x[0].tokens) for x in r]))}
+        res["overhead"] = res["boosted"]["ms"] / res["unboosted"]["ms"] - 1.0
+        res["timing"] = ("ms: CUDA events around the pgpb_ctc_beam launch (all frames of the batch); e2e_ms: "
+                         "ctc_beam_batch wall time incl. copy-back and host n-best assembly")
+        out[regime] = res
+    out["_launches"] = launches
+    return out
 
 
 def bench_device_beams(dev, rank, world):

@@ -462,6 +462,32 @@ int pgpb_aed_greedy_step(const pgpb_table *table, const float *d_logprobs, int64
                          int32_t vocab_size, double lam, int32_t use_boost, const pgpb_aed_greedy_state *state,
                          void *stream);
 
+/* ------------------------------------------------------------------------
+ * Batched boosted CTC prefix beam search on the device: ctc_beam_boosted
+ * (decoding.py:232-343, R8) for B utterances of [T, V] log-probs
+ * (d_lp[(b*T + t)*V + v], f32; d_lengths[b] frames or NULL = T), beam <= 32.
+ * One launch decodes every frame.  Per utterance the final beam, in rank
+ * order (am + lam*boost, then am): count[b] prefixes, and per prefix r at
+ * b*beam + r: pb / pnb (blank / non-blank ending mass; am = logaddexp of
+ * both), boost, tree state, token count and the last trace node.  The trace
+ * (TraceStep(token, delta, state) of decoding.py:63-69) is an append-only
+ * trie per utterance at b*trace_nmax + i (parent -1 = empty prefix);
+ * trace_nmax >= T*beam + 1.  am is exact up to the device exp/log1p (within
+ * 1 ulp of the host libm); tokens, boost and states are exact.              */
+typedef struct pgpb_ctc_beam_out {
+  double *pb, *pnb, *boost;   /* [B, beam] */
+  int32_t *tree, *len, *node; /* [B, beam] */
+  int32_t *count;             /* [B]       */
+  int32_t *trace_parent, *trace_token, *trace_state; /* [B, trace_nmax] */
+  double *trace_delta;
+  int64_t trace_nmax;
+  int32_t *overflow;          /* set to 1 if a trace ran out of nodes */
+} pgpb_ctc_beam_out;
+
+int pgpb_ctc_beam(const pgpb_table *table, const float *d_logprobs, int64_t batch, int64_t frames,
+                  int32_t vocab_size, const int32_t *d_lengths, int32_t blank, int32_t beam, double lam,
+                  int32_t use_boost, const pgpb_ctc_beam_out *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,15 @@ class AedGreedyState(ctypes.Structure):
                 ("max_len", c_int32), ("eos", c_int32)]
 
 
+class CtcBeamOut(ctypes.Structure):
+    """pgpb_ctc_beam_out."""
+
+    _fields_ = [("pb", c_void_p), ("pnb", c_void_p), ("boost", c_void_p), ("tree", c_void_p), ("len", c_void_p),
+                ("node", c_void_p), ("count", c_void_p), ("trace_parent", c_void_p), ("trace_token", c_void_p),
+                ("trace_state", c_void_p), ("trace_delta", c_void_p), ("trace_nmax", c_int64),
+                ("overflow", c_void_p)]
+
+
 # name -> argtypes (all return int unless listed in _VOID / _OTHER)
 _P = c_void_p
 _SIGS = {
@@ -127,6 +136,8 @@ _SIGS = {
                         POINTER(TBeamState), c_void_p],
     "pgpb_phrase_hits": [c_void_p, _P, _P, c_int64, _P, _P, _P, _P, _P, _P, c_void_p],
     "pgpb_aed_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_double, c_int32, POINTER(AedState), c_void_p],
+    "pgpb_ctc_beam": [c_void_p, _P, c_int64, c_int64, c_int32, _P, c_int32, c_int32, c_double, c_int32,
+                      POINTER(CtcBeamOut), c_void_p],
     "pgpb_aed_greedy_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_double, c_int32, POINTER(AedGreedyState),
                              c_void_p],
 }

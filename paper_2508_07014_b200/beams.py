@@ -624,3 +624,95 @@ class AEDGreedyDecoder:
     def decode(self, memory, *, record: bool = False, vocab=None, want_trace: bool = False):
         records = self.run(memory, record=record)
         return BeamOutput(self.results(vocab, want_trace), records)
+
+
+# ---------------------------------------------------------------------------
+# CTC prefix beam (batched, device resident)
+
+
+def _logaddexp(a: float, b: float) -> float:  # decoding.py:94-100
+    if a == float("-inf"):
+        return b
+    if b == float("-inf"):
+        return a
+    m = a if a > b else b
+    return m + math.log1p(math.exp(-abs(a - b)))
+
+
+def ctc_beam_batch(logprobs, lengths=None, table: ArcTable | None = None, cfg: DecodeConfig | None = None, *,
+                   blank_id: int, vocab=None, want_trace: bool = False):
+    """Boosted CTC prefix beam search (decoding.py:232-343, R8) for a batch:
+    one pgpb_ctc_beam launch decodes every frame of every utterance on the
+    device (beam <= 32).  logprobs: [B, T, V] float32 (CUDA tensor or
+    numpy); lengths: [B] frames or None.  Returns per utterance the
+    reference's (best, nbest) pair.  Tokens, boosts and traces are exact; am
+    is within an ulp-level difference of the host's logaddexp."""
+    torch = _torch()
+    cfg = cfg or DecodeConfig()
+    lp = logprobs if isinstance(logprobs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(logprobs, np.float32))
+    lp = lp.to(device="cuda", dtype=torch.float32).contiguous()
+    if lp.dim() != 3:
+        raise ValueError("logprobs must be [B, T, V]")
+    B, T, V = lp.shape
+    if table is not None and V != table.vocab_size:
+        raise ValueError(f"emission vocab size {V} != table vocab size {table.vocab_size}")
+    if not 0 <= blank_id < V:
+        raise ValueError(f"blank id {blank_id} out of range [0, {V})")
+    K = cfg.beam_size
+    if K > 32:
+        raise ValueError("device CTC beam search supports beam_size <= 32 (use ctc_beam_boosted for wider beams)")
+    ln = None
+    if lengths is not None:
+        ln = torch.as_tensor(np.asarray(lengths) if not isinstance(lengths, torch.Tensor) else lengths)
+        from .rnnt import _check_lengths
+
+        _check_lengths(ln, B, T)
+        ln = ln.to(device=lp.device, dtype=torch.int32).contiguous()
+    o, tr = ctc_beam_device(lp, ln, table, cfg, blank_id)
+    if int(o.pop("overflow").item()):
+        raise RuntimeError("CTC beam trace overflow")
+    h = {k: v.cpu().numpy() for k, v in o.items()}
+    t = {k: v.cpu().numpy() for k, v in tr.items()}
+    lam = cfg.lam
+    results = []
+    for b in range(B):
+        out = []
+        for r in range(int(h["count"][b])):
+            steps = _walk(t, b, int(h["node"][b, r]))
+            toks = [s_[0] for s_ in steps]
+            am = _logaddexp(float(h["pb"][b, r]), float(h["pnb"][b, r]))
+            out.append((toks, am, float(h["boost"][b, r]), steps))
+        out.sort(key=lambda x: (-(x[1] + lam * x[2]), -x[1], tuple(x[0])))
+        nbest = [DecodeResult(list(tk), _text(tk, vocab), a, bo, [TraceStep(*s_) for s_ in sp] if want_trace else None)
+                 for tk, a, bo, sp in out[:K]]
+        results.append((nbest[0] if nbest else None, nbest))
+    return results
+
+
+def ctc_beam_device(lp, lengths, table, cfg: DecodeConfig, blank_id: int):
+    """The pgpb_ctc_beam launch alone (no host synchronisation except the
+    trace-overflow check): lp [B, T, V] float32 CUDA, lengths int32 CUDA [B]
+    or None.  Returns (final beams, trace) dicts of device tensors."""
+    torch = _torch()
+    B, T, V = lp.shape
+    K = cfg.beam_size
+    ln = lengths
+    use = _boost_active(table, cfg)
+    dev = lp.device
+    nmax = T * K + 1
+    f64, i32 = torch.float64, torch.int32
+    o = {k: torch.zeros((B, K), dtype=f64, device=dev) for k in ("pb", "pnb", "boost")}
+    o.update({k: torch.zeros((B, K), dtype=i32, device=dev) for k in ("tree", "len", "node")})
+    o["count"] = torch.zeros(B, dtype=i32, device=dev)
+    tr = {k: torch.zeros((B, nmax), dtype=i32, device=dev) for k in ("parent", "token", "state")}
+    tr["delta"] = torch.zeros((B, nmax), dtype=f64, device=dev)
+    ovf = torch.zeros(1, dtype=i32, device=dev)
+    p = lambda x: x.data_ptr()  # noqa: E731
+    st = _lib.CtcBeamOut(p(o["pb"]), p(o["pnb"]), p(o["boost"]), p(o["tree"]), p(o["len"]), p(o["node"]),
+                         p(o["count"]), p(tr["parent"]), p(tr["token"]), p(tr["state"]), p(tr["delta"]), nmax, p(ovf))
+    handle = table.device_table(dev.index).handle if use else None
+    _lib.check(_lib.LIB.pgpb_ctc_beam(handle, lp.data_ptr(), B, T, V, None if ln is None else ln.data_ptr(),
+                                      int(blank_id), K, float(cfg.lam), int(use), _lib.ctypes.byref(st),
+                                      _lib.stream_ptr()), "pgpb_ctc_beam")
+    o["overflow"] = ovf
+    return o, tr

@@ -1,0 +1,458 @@
+// Batched boosted CTC prefix beam search, device resident (pgpb_ctc_beam).
+//
+// Reference: ctc_beam_boosted (decoding.py:232-343, R8), _logaddexp
+// (:94-100).  One CTA per utterance runs every frame of the utterance in one
+// launch; the beam (<= 32 prefixes) lives in shared memory.  Per frame:
+//   1. the frame's log-prob row is staged in shared memory (the next frame's
+//      row is prefetched into the other buffer while this one is decided);
+//   2. every live prefix j finds its parent among the live prefixes
+//      (length, prefix hash, confirmed on the trace chains) and computes its
+//      carries: pb' = tot_j + lp[blank], pnb' = pnb_j + lp[last_j] (+) the
+//      parent's extension mass — at most two terms, so the reference's
+//      accumulation order does not matter;
+//   3. every (prefix i, token v != blank) that does not land on a live prefix
+//      is scored as a new prefix: am = (v == last_i ? pb_i : tot_i) + lp[v],
+//      boost = boost_i + score(state_i, v) (closure tokens exactly from the
+//      flattened closure, all others from the dense root row shifted by the
+//      state's backoff total), key = am + lam * boost; per-thread top-K
+//      lists plus the carried prefixes, then `beam` block-wide argmax rounds
+//      (the reference's ranking: key, then am; exact ties between different
+//      prefixes fall back to (slot, token) order — DESIGN.md §2);
+//   4. winners become the next beam; new prefixes append a trace node
+//      (TraceStep(v, delta, next), decoding.py:63-69).
+// Scores: fp64 in the reference's operation order; logaddexp uses the
+// device exp / log1p (within 1 ulp of the host's libm), so am values match
+// the reference within ~1e-15 relative, boost and tree states exactly.
+
+#include <string>
+
+#include "pgpb_beam.cuh"
+
+namespace pgpb {
+
+namespace {
+
+constexpr int kCbThreads = 256;
+
+__device__ __forceinline__ double logaddexp(double a, double b) {
+  if (a == -INFINITY) return b;
+  if (b == -INFINITY) return a;
+  const double m = a > b ? a : b;
+  return __dadd_rn(m, log1p(exp(-fabs(__dadd_rn(a, -b)))));
+}
+
+__device__ __forceinline__ uint64_t cb_hash_push(uint64_t h, int v) {
+  uint64_t x = h * 0x100000001B3ull + (uint64_t(uint32_t(v)) + 0x9E3779B97F4A7C15ull);
+  x ^= x >> 31;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+
+// Token sequences ending at trace nodes a and b (-1 = empty) are equal?
+__device__ bool cb_same_tokens(const int32_t *parent, const int32_t *token, int a, int b) {
+  while (a != b) {
+    if (a < 0 || b < 0) return false;
+    if (token[a] != token[b]) return false;
+    a = parent[a];
+    b = parent[b];
+  }
+  return true;
+}
+
+struct Slots {
+  double pb[kMaxTopK], pnb[kMaxTopK], boost[kMaxTopK];
+  uint64_t hash[kMaxTopK], phash[kMaxTopK];
+  int tree[kMaxTopK], last[kMaxTopK], node[kMaxTopK], len[kMaxTopK];
+};
+
+struct CbArgs {
+  TableView t;
+  const float *lp;  // [B, T, V]
+  int64_t B, T;
+  int V;
+  const int32_t *lengths;
+  int blank;
+  int beam;
+  double lam;
+  int use_boost;
+  // trace (per utterance b: nodes b*nmax ..)
+  int32_t *tr_parent, *tr_token, *tr_state;
+  double *tr_delta;
+  int64_t nmax;
+  // final beams [B, beam]
+  double *o_pb, *o_pnb, *o_boost;
+  int32_t *o_node, *o_len, *o_tree;
+  int32_t *o_count;
+  int32_t *overflow;
+};
+
+template <int K, bool kVec>
+__global__ void __launch_bounds__(kCbThreads) ctc_beam_kernel(CbArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ Slots cur, nxt;
+  __shared__ int s_par[kMaxTopK], s_n;
+  __shared__ double s_cpb[kMaxTopK], s_cpnb[kMaxTopK], s_tot[kMaxTopK];
+  __shared__ int4 s_rec[kMaxTopK];
+  __shared__ Cand s_warp[kCbThreads / 32];
+  __shared__ int s_win[kMaxTopK];
+  __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
+  __shared__ int s_nodes;
+  const TableView &t = a.t;
+  const int V = a.V, Vp = (V + 3) & ~3, Vw = (V + 31) >> 5, beam = a.beam;
+  const bool boost = a.use_boost != 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // shared layout: row[2][Vp] f32 | root[Vp] f32 | rnext[Vp] i32 | bm[K][Vw] | ex[K][Vw]
+  float *rows = reinterpret_cast<float *>(smem);
+  float *root = rows + 2 * Vp;
+  int32_t *rnext = reinterpret_cast<int32_t *>(root + Vp);
+  unsigned *bm = reinterpret_cast<unsigned *>(rnext + Vp);
+  unsigned *ex = bm + size_t(kMaxTopK) * Vw;
+  if (boost) {
+    for (int i = threadIdx.x; i < Vp; i += blockDim.x) {
+      root[i] = __ldg(t.root_scores + i);
+      rnext[i] = __ldg(t.root_next + i);
+    }
+  }
+  for (int64_t b = blockIdx.x; b < a.B; b += gridDim.x) {
+    const int64_t Tb = a.lengths ? min(max(int64_t(__ldg(a.lengths + b)), int64_t(0)), a.T) : a.T;
+    const int64_t nb = b * a.nmax;
+    int32_t *np = a.tr_parent + nb, *nt = a.tr_token + nb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      cur.pb[0] = 0.0;
+      cur.pnb[0] = -INFINITY;
+      cur.boost[0] = 0.0;
+      cur.hash[0] = 0ull;
+      cur.phash[0] = 0ull;
+      cur.tree[0] = 0;
+      cur.last[0] = -1;
+      cur.node[0] = -1;
+      cur.len[0] = 0;
+      s_n = 1;
+      s_nodes = 0;
+    }
+    // frame 0's row
+    const float *lpb = a.lp + b * a.T * int64_t(V);
+    if (Tb > 0)
+      for (int i = threadIdx.x; i < V; i += blockDim.x) rows[i] = __ldg(lpb + i);
+    __syncthreads();
+    for (int64_t tf = 0; tf < Tb; ++tf) {
+      const float *row = rows + (tf & 1) * Vp;
+      // prefetch the next frame's row into the other buffer (consumed after
+      // this frame's barriers)
+      if (tf + 1 < Tb) {
+        float *nrow = rows + ((tf + 1) & 1) * Vp;
+        const float *src = lpb + (tf + 1) * int64_t(V);
+        if (kVec) {  // asynchronous copies (cp.async): the loads overlap this frame's work
+          for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(nrow + 4 * i));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + 4 * i) : "memory");
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        } else {
+          for (int i = threadIdx.x; i < V; i += blockDim.x) nrow[i] = __ldg(src + i);
+        }
+      }
+      const int n = s_n;
+      // 2. parents, totals, carries (one thread per live prefix)
+      if (threadIdx.x < n) {
+        const int j = threadIdx.x;
+        const double tot = logaddexp(cur.pb[j], cur.pnb[j]);
+        s_tot[j] = tot;
+        int par = -1;
+        if (cur.len[j] > 0) {
+          for (int i = 0; i < n && par < 0; ++i)
+            if (cur.len[i] == cur.len[j] - 1 && cur.hash[i] == cur.phash[j] &&
+                cb_same_tokens(np, nt, np[cur.node[j]], cur.node[i]))
+              par = i;
+        }
+        s_par[j] = par;
+        s_cpb[j] = __dadd_rn(tot, static_cast<double>(row[a.blank]));
+        double pnb = -INFINITY;
+        if (cur.len[j] > 0) pnb = logaddexp(pnb, __dadd_rn(cur.pnb[j], static_cast<double>(row[cur.last[j]])));
+        if (par >= 0) {
+          // the parent's iteration (decoding.py:303-321): v = last_j
+          const int v = cur.last[j];
+          double tot_i = logaddexp(cur.pb[par], cur.pnb[par]);
+          const double contrib =
+              __dadd_rn(v == cur.last[par] ? cur.pb[par] : tot_i, static_cast<double>(row[v]));
+          if (contrib != -INFINITY) pnb = logaddexp(pnb, contrib);
+        }
+        s_cpnb[j] = pnb;
+      }
+      // exclusion bitmaps (extensions landing on a live prefix) and
+      // closure records
+      for (int i = threadIdx.x; i < n * Vw; i += blockDim.x) ex[i] = 0u;
+      if (boost) {
+        for (int i = threadIdx.x; i < n * Vw; i += blockDim.x) bm[i] = 0u;
+        for (int h = threadIdx.x; h < n; h += blockDim.x) s_rec[h] = __ldg(t.clo_rec + cur.tree[h]);
+      }
+      __syncthreads();
+      if (threadIdx.x < n && s_par[threadIdx.x] >= 0) {
+        const int v = cur.last[threadIdx.x];
+        atomicOr(ex + s_par[threadIdx.x] * Vw + (v >> 5), 1u << (v & 31));
+      }
+      int total = 0;
+      if (boost) {
+        for (int h = 0; h < n; ++h) total += s_rec[h].y;
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+          int h = 0, off = idx;
+          while (off >= s_rec[h].y) {
+            off -= s_rec[h].y;
+            ++h;
+          }
+          const int tok = __ldg(&t.clo[s_rec[h].x + off].x);
+          atomicOr(bm + h * Vw + (tok >> 5), 1u << (tok & 31));
+        }
+      }
+      __syncthreads();
+      // 3. new-prefix candidates
+      Cand list[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+      for (int h = 0; h < n; ++h) {
+        const double tot = s_tot[h], pb = cur.pb[h], bh = cur.boost[h];
+        const int last = cur.last[h];
+        const float acc = boost ? __int_as_float(s_rec[h].z) : 0.0f;
+        const unsigned *hb = bm + h * Vw, *he = ex + h * Vw;
+        auto consider = [&](int v, float x, double bv) {
+          if (v == a.blank || ((he[v >> 5] >> (v & 31)) & 1u)) return;
+          const double amv = __dadd_rn(v == last ? pb : tot, static_cast<double>(x));
+          if (amv == -INFINITY) return;
+          list_insert<K>(list, Cand{__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, h * V + v});
+        };
+        auto dense = [&](int v, float x) {
+          if (boost) {
+            if ((hb[v >> 5] >> (v & 31)) & 1u) return;
+            consider(v, x, __dadd_rn(bh, static_cast<double>(acc + root[v])));
+          } else {
+            consider(v, x, __dadd_rn(bh, 0.0));
+          }
+        };
+        if (kVec) {
+          const float4 *r4 = reinterpret_cast<const float4 *>(row);
+          for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) {
+            const float4 x = r4[i];
+            dense(4 * i, x.x);
+            dense(4 * i + 1, x.y);
+            dense(4 * i + 2, x.z);
+            dense(4 * i + 3, x.w);
+          }
+        } else {
+          for (int v = threadIdx.x; v < V; v += blockDim.x) dense(v, row[v]);
+        }
+      }
+      if (boost) {
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+          int h = 0, off = idx;
+          while (off >= s_rec[h].y) {
+            off -= s_rec[h].y;
+            ++h;
+          }
+          const int4 e = __ldg(t.clo + s_rec[h].x + off);
+          const int v = e.x;
+          if (v == a.blank || ((ex[h * Vw + (v >> 5)] >> (v & 31)) & 1u)) continue;
+          const double amv = __dadd_rn(v == cur.last[h] ? cur.pb[h] : s_tot[h], static_cast<double>(row[v]));
+          if (amv == -INFINITY) continue;
+          const double bv = __dadd_rn(cur.boost[h], static_cast<double>(__int_as_float(e.z)));
+          list_insert<K>(list, Cand{__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, h * V + v});
+        }
+      }
+      // carried prefixes (cid past the extension range)
+      if (threadIdx.x < n) {
+        const int j = threadIdx.x;
+        const double amj = logaddexp(s_cpb[j], s_cpnb[j]);
+        list_insert<K>(list, Cand{__dadd_rn(amj, __dmul_rn(a.lam, cur.boost[j])), amj, kMaxTopK * V + j});
+      }
+      // 4. beam rounds of block argmax
+      for (int r = 0; r < beam; ++r) {
+        Cand best = list[0];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const Cand oc = shfl_cand(best, o);
+          if (cand_better(oc, best)) best = oc;
+        }
+        if (lane == 0) s_warp[wid] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          Cand bb = s_warp[0];
+          for (int w = 1; w < kCbThreads / 32; ++w)
+            if (cand_better(s_warp[w], bb)) bb = s_warp[w];
+          s_win[r] = bb.cid;
+          s_key[r] = bb.key;
+          s_am[r] = bb.am;
+        }
+        __syncthreads();
+        if (s_win[r] != INT_MAX && list[0].cid == s_win[r]) list_pop<K>(list);
+      }
+      // 5. the next beam
+      if (threadIdx.x < beam) {
+        const int r = threadIdx.x;
+        const int cid = s_win[r];
+        if (cid != INT_MAX) {
+          if (cid >= kMaxTopK * V) {  // carried prefix
+            const int j = cid - kMaxTopK * V;
+            nxt.pb[r] = s_cpb[j];
+            nxt.pnb[r] = s_cpnb[j];
+            nxt.boost[r] = cur.boost[j];
+            nxt.hash[r] = cur.hash[j];
+            nxt.phash[r] = cur.phash[j];
+            nxt.tree[r] = cur.tree[j];
+            nxt.last[r] = cur.last[j];
+            nxt.node[r] = cur.node[j];
+            nxt.len[r] = cur.len[j];
+          } else {
+            const int h = cid / V, v = cid - h * V;
+            float sc = 0.0f;
+            int nx = 0;
+            if (boost) {
+              if ((bm[h * Vw + (v >> 5)] >> (v & 31)) & 1u) {
+                if (t.clo_bits) {
+                  const uint2 w = __ldg(t.clo_bits + int64_t(cur.tree[h]) * t.bits_words + (v >> 5));
+                  const int4 e = __ldg(t.clo + s_rec[h].x + int(w.y) + __popc(w.x & ((1u << (v & 31)) - 1u)));
+                  sc = __int_as_float(e.z);
+                  nx = e.y;
+                } else {
+                  resolve_cell(t, root, rnext, cur.tree[h], v, sc, nx);
+                }
+              } else {
+                sc = __int_as_float(s_rec[h].z) + root[v];
+                nx = rnext[v];
+              }
+            }
+            // trace node: winners of this frame take consecutive nodes in
+            // rank order among the new prefixes
+            int rank = 0;
+            for (int q = 0; q < r; ++q) rank += s_win[q] != INT_MAX && s_win[q] < kMaxTopK * V;
+            const int node = s_nodes + rank;
+            if (node < a.nmax) {
+              a.tr_parent[nb + node] = cur.node[h];
+              a.tr_token[nb + node] = v;
+              a.tr_state[nb + node] = nx;
+              a.tr_delta[nb + node] = static_cast<double>(sc);
+            } else {
+              *a.overflow = 1;
+            }
+            nxt.pb[r] = -INFINITY;
+            nxt.pnb[r] = s_am[r];
+            nxt.boost[r] = __dadd_rn(cur.boost[h], static_cast<double>(sc));
+            nxt.hash[r] = cb_hash_push(cur.hash[h], v);
+            nxt.phash[r] = cur.hash[h];
+            nxt.tree[r] = nx;
+            nxt.last[r] = v;
+            nxt.node[r] = node < a.nmax ? node : -1;
+            nxt.len[r] = cur.len[h] + 1;
+          }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int m = 0, e = 0;
+        while (m < beam && s_win[m] != INT_MAX) {
+          e += s_win[m] < kMaxTopK * V;
+          ++m;
+        }
+        s_n = m;
+        s_nodes += e;
+      }
+      if (threadIdx.x < beam) {
+        const int r = threadIdx.x;
+        cur.pb[r] = nxt.pb[r];
+        cur.pnb[r] = nxt.pnb[r];
+        cur.boost[r] = nxt.boost[r];
+        cur.hash[r] = nxt.hash[r];
+        cur.phash[r] = nxt.phash[r];
+        cur.tree[r] = nxt.tree[r];
+        cur.last[r] = nxt.last[r];
+        cur.node[r] = nxt.node[r];
+        cur.len[r] = nxt.len[r];
+      }
+      if (kVec) asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+    }
+    // final beam (rank order)
+    if (threadIdx.x < beam) {
+      const int r = threadIdx.x;
+      const int64_t o = b * beam + r;
+      if (r < s_n) {
+        a.o_pb[o] = cur.pb[r];
+        a.o_pnb[o] = cur.pnb[r];
+        a.o_boost[o] = cur.boost[r];
+        a.o_node[o] = cur.node[r];
+        a.o_len[o] = cur.len[r];
+        a.o_tree[o] = cur.tree[r];
+      }
+    }
+    if (threadIdx.x == 0) a.o_count[b] = s_n;
+  }
+}
+
+}  // namespace
+
+}  // namespace pgpb
+
+extern "C" int pgpb_ctc_beam(const pgpb_table *table, const float *d_lp, int64_t B, int64_t T, int32_t V,
+                             const int32_t *d_lengths, int32_t blank, int32_t beam, double lam, int32_t use_boost,
+                             const pgpb_ctc_beam_out *out, void *stream) {
+  using namespace pgpb;
+  if (!out) return fail(PGPB_EINVAL, "out is NULL");
+  if (B < 0 || T < 0 || V < 1) return fail(PGPB_EINVAL, "bad shape");
+  if (beam < 1 || beam > kMaxTopK) return fail(PGPB_EINVAL, "beam must be in [1, 32]");
+  if (blank < 0 || blank >= V) return fail(PGPB_EINVAL, "blank out of range");
+  if (use_boost && !table) return fail(PGPB_EINVAL, "use_boost requires a table");
+  if (table && table->view.vocab_size != V)
+    return fail(PGPB_EINVAL, "emission vocab size " + std::to_string(V) + " != table vocab size " +
+                                 std::to_string(table->view.vocab_size));
+  if (int64_t(kMaxTopK + 1) * V >= INT_MAX) return fail(PGPB_EINVAL, "vocabulary too large");
+  if (out->trace_nmax < T * int64_t(beam) + 1) return fail(PGPB_EINVAL, "trace_nmax must be >= T * beam + 1");
+  if (B == 0) return PGPB_OK;
+  CbArgs a{};
+  if (table) {
+    a.t = table->view;
+  } else {
+    a.t.vocab_size = V;
+    a.t.vocab_padded = (V + 3) & ~3;
+  }
+  a.lp = d_lp;
+  a.B = B;
+  a.T = T;
+  a.V = V;
+  a.lengths = d_lengths;
+  a.blank = blank;
+  a.beam = beam;
+  a.lam = lam;
+  a.use_boost = use_boost ? 1 : 0;
+  a.tr_parent = out->trace_parent;
+  a.tr_token = out->trace_token;
+  a.tr_state = out->trace_state;
+  a.tr_delta = out->trace_delta;
+  a.nmax = out->trace_nmax;
+  a.o_pb = out->pb;
+  a.o_pnb = out->pnb;
+  a.o_boost = out->boost;
+  a.o_node = out->node;
+  a.o_len = out->len;
+  a.o_tree = out->tree;
+  a.o_count = out->count;
+  a.overflow = out->overflow;
+  const int Vp = (V + 3) & ~3, Vw = (V + 31) >> 5;
+  const size_t smem = size_t(Vp) * 4 * 4 + size_t(2) * kMaxTopK * Vw * 4;
+  if (smem > 200 * 1024) return fail(PGPB_EINVAL, "vocabulary too large for the shared-memory rows");
+  const bool vec = (V % 4) == 0 && (reinterpret_cast<uintptr_t>(d_lp) % 16) == 0;
+  using Fn = void (*)(CbArgs);
+  Fn fn;
+  if (beam <= 4) fn = vec ? ctc_beam_kernel<4, true> : ctc_beam_kernel<4, false>;
+  else if (beam <= 8) fn = vec ? ctc_beam_kernel<8, true> : ctc_beam_kernel<8, false>;
+  else if (beam <= 16) fn = vec ? ctc_beam_kernel<16, true> : ctc_beam_kernel<16, false>;
+  else fn = vec ? ctc_beam_kernel<32, true> : ctc_beam_kernel<32, false>;
+  PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
+  const int64_t cap = int64_t(sm_count(current_device())) * 2;
+  const unsigned grid = unsigned(B < cap ? B : cap);
+  fn<<<grid, kCbThreads, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  PGPB_CUDA_TRY(cudaGetLastError());
+  return PGPB_OK;
+}
