@@ -363,8 +363,9 @@ __global__ void __launch_bounds__(kThreads, 4)
 // the same closure lookup the row's output holds at column tok.
 //
 // A work item is (row, part): the row's V/4 float4 chunks split into P
-// equal parts, so a batch smaller than the grid's warps (B=1024 on one of 8
-// GPUs) still keeps every warp streaming.  A warp runs all R steps of its
+// equal parts (64 chunks each by default), so a batch smaller than the
+// grid's warps (B=1024 on one of 8 GPUs) still keeps every warp streaming
+// and every warp has several items to overlap.  A warp runs all R steps of its
 // item with a one-step lookahead: step k+1's closure record, its part of
 // the table's ranked closure bitmap row and the bitmap word of tok_{k+1}
 // are loaded before step k's row is streamed, so their latency hides behind
@@ -399,8 +400,9 @@ __global__ void __launch_bounds__(kThreads, 4)
     int s = __ldg(states + b);
     int4 rec = __ldg(t.clo_rec + s);
     uint2 wb = lane < WP ? __ldg(t.clo_bits + int64_t(s) * Vw + p * WP + lane) : make_uint2(0u, 0u);
-    int tok = __ldg(tokens + b);
-    uint2 tw = __ldg(t.clo_bits + int64_t(s) * Vw + (tok >> 5));
+    // tokens == NULL: a single advance (R = 1), no successor
+    int tok = tokens ? __ldg(tokens + b) : 0;
+    uint2 tw = tokens ? __ldg(t.clo_bits + int64_t(s) * Vw + (tok >> 5)) : make_uint2(0u, 0u);
     if (!triggered) {
       asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       triggered = true;
@@ -409,8 +411,10 @@ __global__ void __launch_bounds__(kThreads, 4)
       // successor of this step (uniform across the warp): closure entry by
       // rank when tok is a first-hit arc of s, else the dense root row
       const unsigned bp = unsigned(tok) & 31u;
-      int sn;
-      if ((tw.x >> bp) & 1u)
+      int sn = s;
+      if (!tokens)
+        ;
+      else if ((tw.x >> bp) & 1u)
         sn = __ldg(&t.clo[rec.x + int(tw.y) + __popc(tw.x & ((1u << bp) - 1u))].y);
       else
         sn = s_next[tok];
@@ -577,19 +581,19 @@ static int launch_advance(const pgpb_table *table, const int32_t *d_states, int6
   return PGPB_OK;
 }
 
-// Parts per row for the chained kernel: valid P (V % (128 P) == 0, Vw <= 32 P)
-// with the best balance of B*P items over the grid's warps (fewest parts on
-// ties).  0 when no P is valid.
-static int steps_parts(const TableView &t, int64_t B, int64_t warps) {
-  int best = 0;
-  double best_eff = -1.0;
+// Parts per row for the chained kernel: 64 float4 chunks per part (two per
+// lane), the measured best at every batch (scripts/advance_steps_sweep.py,
+// V=1024: P=4 gives 74% / 90% / 91% of the HBM peak at B=1024 / 8192 / 65536
+// against 50% / 84% / 85% for whole rows and 54-67% for P=8), or the
+// nearest valid P.  0 when no P is valid.
+static int steps_parts(const TableView &t) {
+  const int want = std::max(1, t.vocab_size / 256);
+  int best = 0, dist = 1 << 30;
   for (int P = 1; P <= 32; P <<= 1) {
     if (t.vocab_size % (128 * P) != 0 || t.bits_words > 32 * P) continue;
-    const int64_t items = B * P;
-    const int64_t rounds = (items + warps - 1) / warps;
-    const double eff = double(items) / double(rounds * warps);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
+    const int d = P > want ? P - want : want - P;
+    if (d < dist) {
+      dist = d;
       best = P;
     }
   }
@@ -602,7 +606,8 @@ static int launch_advance_steps(const pgpb_table *table, const int32_t *d_states
   if (!table) return fail(PGPB_EINVAL, "table is NULL");
   if (B < 0 || R < 0) return fail(PGPB_EINVAL, "batch and steps must be >= 0");
   if (B == 0 || R == 0) return PGPB_OK;
-  if (!d_states || !d_tokens || !d_scores || !d_next) return fail(PGPB_EINVAL, "NULL buffer");
+  if (!d_states || !d_scores || !d_next) return fail(PGPB_EINVAL, "NULL buffer");
+  if (!d_tokens && R != 1) return fail(PGPB_EINVAL, "tokens are required for more than one step");
   const TableView &t = table->view;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nsm = sm_count(current_device());
@@ -610,8 +615,7 @@ static int launch_advance_steps(const pgpb_table *table, const int32_t *d_states
   const bool aligned = (reinterpret_cast<uintptr_t>(d_scores) % 16) == 0 &&
                        (reinterpret_cast<uintptr_t>(d_next) % 16) == 0;
   const int per_sm = 4;
-  const int64_t full_warps = int64_t(nsm) * per_sm * kWarpsPerBlock;
-  int P = parts > 0 ? parts : steps_parts(t, B, full_warps);
+  int P = parts > 0 ? parts : steps_parts(t);
   const bool ok = P > 0 && t.clo_bits && aligned && root_bytes <= 64 * 1024 &&
                   t.vocab_size % (128 * P) == 0 && t.bits_words <= 32 * P;
   if (ok) {
@@ -647,6 +651,7 @@ static int launch_advance_steps(const pgpb_table *table, const int32_t *d_states
     }
     rc = launch_advance(table, src, B, d_scores + k * cells, d_next + k * cells, stream, false);
     if (rc != PGPB_OK) break;
+    if (!d_tokens) break;  // single advance, no successor
     int32_t *dst = (k + 1 == R && d_final) ? d_final : bufs[k & 1];
     gather_next_kernel<<<g, 256, 0, st>>>(d_next + k * cells, d_tokens + int64_t(k) * B, B, t.vocab_size, dst);
     if (cudaGetLastError() != cudaSuccess) rc = fail(PGPB_ECUDA, "gather_next_kernel launch failed");
