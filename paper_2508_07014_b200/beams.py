@@ -167,6 +167,36 @@ class StatelessTransducerModel:
     def project_encoder(self, enc):
         return enc.to(self.dtype) @ self.w_enc.T
 
+    def align(self, beta: float = 3.0, gamma: float = 1.0):
+        """Structured init of the prediction table for a transducer-like
+        alignment behaviour (benchmarks): every context adds beta * relu(w_out
+        [blank]) to the joint hidden (blank likely once the frame's token has
+        been emitted) and a token context subtracts gamma * w_out[token]
+        (repeating it is unlikely), so a frame that favours token y emits y
+        once and then blanks, as a trained transducer does.  The random part
+        of the table is kept."""
+        torch = _torch()
+        W = self.w_out.float()
+        off = beta * torch.relu(W[self.blank_id]).unsqueeze(0) - gamma * W
+        off[self.blank_id] = beta * torch.relu(W[self.blank_id])
+        self.pred_j = (self.pred_j.float() + off).to(self.dtype)
+        return self
+
+    def aligned_frames(self, tokens_per_frame, alpha: float = 4.0, alpha_blank: float = 2.5, noise: float = 0.1,
+                       generator=None):
+        """Synthetic projected encoder frames [B, T, J]: a frame with target
+        token y (>= 0) is alpha * relu(w_out[y]), a blank frame (-1)
+        alpha_blank * relu(w_out[blank]), plus N(0, noise)."""
+        torch = _torch()
+        tpf = torch.as_tensor(tokens_per_frame, device=self.w_out.device).long()
+        W = torch.relu(self.w_out.float())
+        idx = torch.where(tpf < 0, torch.full_like(tpf, self.blank_id), tpf)
+        scale = torch.where(tpf < 0, torch.full(tpf.shape, alpha_blank, device=tpf.device),
+                            torch.full(tpf.shape, alpha, device=tpf.device))
+        e = W[idx] * scale.unsqueeze(-1)
+        e = e + noise * torch.randn(e.shape, device=e.device, generator=generator)
+        return e.to(self.dtype)
+
     def joint_logprobs(self, enc_t, last):
         """enc_t [B, J] (each utterance's frame), last [B, K] int (-1 = start) -> [B*K, V] f32."""
         torch = _torch()

@@ -24,9 +24,16 @@ phrases, V = gi.corpus("p20k_v1024")
 ctx = pb.ContextList([pb.Phrase(" ".join(map(str, p)), p) for p in phrases], min_chars=0)
 tab = pb.compile_arc_table(pb.compute_fail_links(pb.build_prefix_tree(ctx, pb.TreeParams(), V)))
 vocab = Vocabulary(tokens=tuple(str(i) for i in range(V)), blank_id=0)
-targets, seeds, _ = gi.reference_overhead_corpus()
-ems = [synth_ctc_emissions(tg, vocab, margin=0.5, seed=sd, boost_positions=[], blanks_between=3).logprobs
-       for tg, sd in zip(targets, seeds)]
+if len(sys.argv) > 1 and sys.argv[1] == "clean200":  # the bench's clean regime shape
+    rng = np.random.default_rng(4242)
+    targets = [[int(x) for x in rng.integers(1, V, size=51)] for _ in range(128)]
+    seeds = [int(rng.integers(2**31)) for _ in range(128)]
+    ems = [synth_ctc_emissions(tg, vocab, margin=0.5, seed=sd, boost_positions=[], blanks_between=3).logprobs[:200]
+           for tg, sd in zip(targets, seeds)]
+else:
+    targets, seeds, _ = gi.reference_overhead_corpus()
+    ems = [synth_ctc_emissions(tg, vocab, margin=0.5, seed=sd, boost_positions=[], blanks_between=3).logprobs
+           for tg, sd in zip(targets, seeds)]
 lens = np.array([e.shape[0] for e in ems], np.int32)
 pad = np.zeros((len(ems), int(lens.max()), V), np.float32)
 for i, e in enumerate(ems):

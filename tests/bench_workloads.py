@@ -9,10 +9,12 @@ from __future__ import annotations
 
 from functools import lru_cache
 
+import numpy as np
+
 import gen_inputs as gi
 
 C2 = dict(B=128, T=200, D=512, pred=640, joint=640, blank_bias=10.5, corpus="p20k_v1024")
-C3 = dict(B=64, T=200, D=512, pred=640, joint=640, blank_bias=4.0, beam=4, cap=5, corpus="p5k_v1024")
+C3 = dict(B=64, T=200, D=512, pred=640, joint=640, beam=4, cap=5, corpus="p5k_v1024")
 C4 = dict(B=64, Tm=100, d=256, layers=4, heads=4, ff=1024, max_len=48, beam=4, eos_bias=-4.0, eos_ramp=0.4,
           corpus="p20k_v4096")
 
@@ -43,19 +45,46 @@ def config2(dev, rank: int = 0):
     return model, tab, enc_proj
 
 
+def config3_targets(rng, V, T, phrases, emit_rate=0.3, phrase_frac=0.6):
+    """Per-frame targets of one synthetic utterance: about emit_rate of the
+    frames carry a token (config 2's 0.3 tokens per frame), the rest are
+    blank (-1); the token stream is a mix of key phrases from the tree's
+    corpus (phrase_frac of the tokens) and random filler, so boosted beams
+    walk deep tree states."""
+    n = int(round(emit_rate * T))
+    toks = []
+    while len(toks) < n:
+        if rng.random() < phrase_frac:
+            toks.extend(int(x) for x in phrases[int(rng.integers(len(phrases)))])
+        else:
+            toks.extend(int(x) for x in rng.integers(1, V, size=int(rng.integers(1, 4))))
+    toks = toks[:n]
+    frames = np.full(T, -1, np.int64)
+    pos = np.sort(rng.choice(T, size=n, replace=False))
+    frames[pos] = toks
+    return frames
+
+
 def config3(dev, rank: int = 0):
-    """RNN-T beam 4: stateless pred net + joint, 5K tree, 64 x 200 frames."""
+    """RNN-T beam 4: stateless pred net + joint (random init, aligned
+    structure: StatelessTransducerModel.align), 5K tree, 64 x 200 frames of
+    synthetic projected encoder output with ~0.3 tokens per frame drawn from
+    the tree's key phrases and filler (config3_targets)."""
+    import numpy as np
     import torch
 
     from paper_2508_07014_b200.beams import StatelessTransducerModel
 
     c = C3
     tab, V = table(c["corpus"])
+    phrases, _ = gi.corpus(c["corpus"])
     model = StatelessTransducerModel(V, enc_dim=c["D"], pred_dim=c["pred"], joint_dim=c["joint"], seed=3 + rank,
-                                     blank_bias=c["blank_bias"])
+                                     blank_bias=0.0).align()
+    rng = np.random.default_rng(77 + rank)
+    tpf = np.stack([config3_targets(rng, V, c["T"], phrases) for _ in range(c["B"])])
     g = torch.Generator(device=dev)
     g.manual_seed(77 + rank)
-    enc_proj = model.project_encoder(torch.randn((c["B"], c["T"], c["D"]), generator=g, device=dev))
+    enc_proj = model.aligned_frames(torch.from_numpy(tpf).to(dev), generator=g)
     return model, tab, enc_proj
 
 
