@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kBeamThreads) beam_topk_kernel(BeamArgs a) {
       const int64_t h = h0 + hl;
       float s = 0.0f;
       int nx = 0;
-      if (a.use_boost) resolve_cell(t, root, rnext, a.states[h], v, s, nx);
+      if (a.use_boost) resolve_ranked(t, root, bm + hl * bm_words, __ldg(t.clo_rec + a.states[h]), v, s, nx);
       a.out_hyp[o] = static_cast<int32_t>(h);
       a.out_token[o] = v;
       a.out_am[o] = s_win_am[r];

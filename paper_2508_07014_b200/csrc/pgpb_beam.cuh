@@ -71,4 +71,25 @@ __device__ __forceinline__ void resolve_cell(const TableView &t, const float *ro
   }
 }
 
+// Resolve (score, next) of token v at a state whose closure tokens are set
+// in the shared-memory bitmap bm_h (its closure record rec, loaded already):
+// a closure token's entry is the rank(v)-th of the state's sorted closure
+// (popcounts over the bitmap), so the lookup costs one load instead of the
+// binary search's dependent chain; a dense token reads the root row.
+__device__ __forceinline__ void resolve_ranked(const TableView &t, const float *root, const unsigned *bm_h,
+                                               const int4 &rec, int v, float &s, int &nx) {
+  const int wv = v >> 5;
+  const unsigned w = bm_h[wv];
+  if ((w >> (v & 31)) & 1u) {
+    int rank = __popc(w & ((1u << (v & 31)) - 1u));
+    for (int q = 0; q < wv; ++q) rank += __popc(bm_h[q]);
+    const int4 e = __ldg(t.clo + rec.x + rank);
+    s = __int_as_float(e.z);
+    nx = e.y;
+  } else {
+    s = __int_as_float(rec.z) + root[v];
+    nx = __ldg(t.root_next + v);
+  }
+}
+
 }  // namespace pgpb

@@ -308,21 +308,7 @@ __global__ void __launch_bounds__(kCbThreads) ctc_beam_kernel(CbArgs a) {
             const int h = cid / V, v = cid - h * V;
             float sc = 0.0f;
             int nx = 0;
-            if (boost) {
-              if ((bm[h * Vw + (v >> 5)] >> (v & 31)) & 1u) {
-                if (t.clo_bits) {
-                  const uint2 w = __ldg(t.clo_bits + int64_t(cur.tree[h]) * t.bits_words + (v >> 5));
-                  const int4 e = __ldg(t.clo + s_rec[h].x + int(w.y) + __popc(w.x & ((1u << (v & 31)) - 1u)));
-                  sc = __int_as_float(e.z);
-                  nx = e.y;
-                } else {
-                  resolve_cell(t, root, rnext, cur.tree[h], v, sc, nx);
-                }
-              } else {
-                sc = __int_as_float(s_rec[h].z) + root[v];
-                nx = rnext[v];
-              }
-            }
+            if (boost) resolve_ranked(t, root, bm + h * Vw, s_rec[h], v, sc, nx);
             // trace node: winners of this frame take consecutive nodes in
             // rank order among the new prefixes
             int rank = 0;

@@ -270,8 +270,57 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
   if (threadIdx.x == 0) s_node_base = S.trace.count[b];
   __syncthreads();
 
-  // 1. blank extensions -> finished pool, in rank (slot) order (warp 0)
-  if (threadIdx.x < 32) {
+  // 1. blank extensions -> finished pool, in rank (slot) order (warp 0).
+  // Pools of <= 32 entries live in the warp's registers (lane j = entry j,
+  // loaded once), so each slot's merge is a ballot instead of a global round
+  // trip; larger pools take the general loop below.
+  if (threadIdx.x < 32 && S.pool_cap <= 32) {
+    const int lane = threadIdx.x;
+    const int64_t pb = int64_t(b) * S.pool_cap;
+    int cnt = S.pool_count[b];
+    int e_len = -1;
+    uint64_t e_hash = 0;
+    double e_am = 0.0, e_bo = 0.0;
+    int e_node = -1;
+    if (lane < cnt) {
+      e_len = S.pool.len[pb + lane];
+      e_hash = S.pool.hash[pb + lane];
+      e_am = S.pool.am[pb + lane];
+      e_bo = S.pool.boost[pb + lane];
+      e_node = S.pool.node[pb + lane];
+    }
+    for (int h = 0; h < beam; ++h) {
+      if (!(s.flags[h] & kValid)) continue;
+      const double am_e = __dadd_rn(s.am[h], static_cast<double>(__ldg(a.lp + (hb + h) * a.ld + a.blank)));
+      const double bo_e = s.boost[h];
+      bool eq = false;
+      if (lane < cnt && e_len == s.len[h] && e_hash == s.hash[h]) eq = same_tokens(np, nt, e_node, s.node[h]);
+      const unsigned m = __ballot_sync(kFull, eq);
+      const int match = m ? __ffs(m) - 1 : -1;
+      int dst = -1;
+      if (match >= 0) {
+        const double oa = __shfl_sync(kFull, e_am, match), ob = __shfl_sync(kFull, e_bo, match);
+        const double ok = rank_key(oa, ob, a.lam);
+        const double ck = rank_key(am_e, bo_e, a.lam);
+        if (ck > ok || (ck == ok && am_e > oa)) dst = match;  // decoding.py:396-404
+      } else if (cnt < S.pool_cap) {
+        dst = cnt;
+      }
+      if (dst >= 0) {
+        if (lane == dst) {
+          e_len = s.len[h];
+          e_hash = s.hash[h];
+          e_am = am_e;
+          e_bo = bo_e;
+          e_node = s.node[h];
+        }
+        if (lane == 0)
+          write_hyp(S.pool, pb + dst, am_e, bo_e, s.tree[h], s.last[h], s.node[h], s.len[h], s.hash[h], kValid);
+      }
+      if (match < 0 && cnt < S.pool_cap) ++cnt;
+    }
+    if (lane == 0) S.pool_count[b] = cnt;
+  } else if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     const int64_t pb = int64_t(b) * S.pool_cap;
     int cnt = S.pool_count[b];
@@ -327,7 +376,7 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
       const int h = cid / V, v = cid % V;
       float sc = 0.0f;
       int nx = 0;
-      if (use_boost) resolve_cell(tv, tv.root_scores, tv.root_next, s.tree[h], v, sc, nx);
+      if (use_boost) resolve_ranked(tv, root, bm + h * ((V + 31) >> 5), s_rec[h], v, sc, nx);
       const int node = s_node_base + r;  // winners fill slots 0.. contiguously
       if (node >= S.trace.nmax) {
         *S.trace.overflow = 1;
@@ -515,7 +564,7 @@ __global__ void __launch_bounds__(kBeamThreads) aed_step_kernel(AedArgs a) {
     } else {
       float sc = 0.0f;
       int nx = 0;
-      if (use_boost) resolve_cell(tv, tv.root_scores, tv.root_next, s.tree[h], v, sc, nx);
+      if (use_boost) resolve_ranked(tv, root, bm + h * bm_words, s_rec[h], v, sc, nx);
       S.trace.state[nb + node] = nx;
       S.trace.delta[nb + node] = static_cast<double>(sc);
       write_hyp(S.hyps, o, s_am[r], __dadd_rn(s.boost[h], static_cast<double>(sc)), nx, v, node, s.len[h] + 1,
