@@ -27,6 +27,35 @@ namespace pgpb {
 
 constexpr uint8_t kValid = 1, kEnded = 2;
 
+// Threads per CTA of the device-beam kernels: small lists (K <= 4) run 1024
+// threads (4 candidates per thread at beam 4 x V 1024: the scan's fp64 key
+// and list-insertion chains are latency-bound, so more warps per SM hide
+// them); K = 8 runs 512 and larger lists 256 (register budget: 64 per thread
+// at 1024 threads).
+template <int K>
+constexpr int db_threads() {
+  return K <= 4 ? 1024 : (K <= 8 ? 512 : 256);
+}
+constexpr int kDbMaxWarps = 32;
+
+#ifdef PGPB_TBEAM_PROFILE
+// Debug build only: per-phase cycles of the transducer wave (CTA 0,
+// thread 0 timeline, summed over launches), read by pgpb_debug_tbeam_profile.
+__device__ unsigned long long g_tb_prof[16];
+#define TB_MARK(i)                                                                  \
+  do {                                                                              \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                      \
+      const long long now_ = clock64();                                             \
+      atomicAdd(&g_tb_prof[i], (unsigned long long)(now_ - tb_last));             \
+      tb_last = now_;                                                               \
+    }                                                                               \
+  } while (0)
+#else
+#define TB_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 __device__ __forceinline__ uint64_t hash_push(uint64_t h, int v) {
   uint64_t x = h * 0x100000001B3ull + (uint64_t(uint32_t(v)) + 0x9E3779B97F4A7C15ull);
   x ^= x >> 31;
@@ -82,46 +111,53 @@ template <int K, bool kVec>
 __device__ __forceinline__ void scan_candidates(const TableView &t, const float *root, const unsigned *bm,
                                                 int bm_words, const float *lp, int64_t ld, int64_t row0, int V,
                                                 const SBeam &s, const bool *expand, int beam, int skip, int special,
-                                                double lam, bool use_boost, const int4 *s_rec, Cand (&list)[K]) {
-  for (int h = 0; h < beam; ++h) {
-    if (!expand[h]) continue;
-    const float *row = lp + (row0 + h) * ld;
+                                                double lam, bool use_boost, const int4 *s_rec, Cand (&list)[K],
+                                                int t0 = 0) {
+  const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
+  // candidate (h, v) of token v at log-prob x (per-slot values from shared memory)
+  auto dense = [&](int h, int v, float x) {
+    if (v == skip) return;
     const double am_h = s.am[h], boost_h = s.boost[h];
-    float acc = 0.0f;
-    int4 rec = make_int4(0, 0, 0, 0);
-    if (use_boost) {
-      rec = s_rec[h];  // loaded by mark_closures
-      acc = __int_as_float(rec.z);
-    }
-    const unsigned *hbm = bm + h * bm_words;
-    auto consider = [&](int v, float x, double bv) {
-      const double amv = __dadd_rn(am_h, static_cast<double>(x));
-      list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + v});
-    };
-    auto dense = [&](int v, float x) {
-      if (v == skip) return;
-      if (v == special) {
-        consider(v, x, __dadd_rn(boost_h, s.extra[h]));
-        return;
-      }
-      if (use_boost) {
-        if ((hbm[v >> 5] >> (v & 31)) & 1u) return;
-        consider(v, x, __dadd_rn(boost_h, static_cast<double>(acc + root[v])));
-      } else {
-        consider(v, x, boost_h);
-      }
-    };
-    if (kVec) {
-      const float4 *row4 = reinterpret_cast<const float4 *>(row);
-      for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) {
-        const float4 x4 = __ldg(row4 + i);
-        dense(4 * i, x4.x);
-        dense(4 * i + 1, x4.y);
-        dense(4 * i + 2, x4.z);
-        dense(4 * i + 3, x4.w);
-      }
+    double bv;
+    if (v == special) {
+      bv = __dadd_rn(boost_h, s.extra[h]);
+    } else if (use_boost) {
+      if ((bm[h * bm_words + (v >> 5)] >> (v & 31)) & 1u) return;
+      bv = __dadd_rn(boost_h, static_cast<double>(__int_as_float(s_rec[h].z) + root[v]));
     } else {
-      for (int v = threadIdx.x; v < V; v += blockDim.x) dense(v, __ldg(row + v));
+      bv = boost_h;
+    }
+    const double amv = __dadd_rn(am_h, static_cast<double>(x));
+    list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + v});
+  };
+  if (kVec) {
+    // work items (slot, float4 chunk) spread over every thread; up to four
+    // items' loads in flight before any is scored
+    const int V4 = V >> 2;
+    const int n = beam * V4;
+    for (int i0 = tid; i0 < n; i0 += 4 * nt) {
+      float4 xs[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int it = i0 + g * nt, h = it / V4;
+        if (it < n && expand[h]) xs[g] = __ldg(reinterpret_cast<const float4 *>(lp + (row0 + h) * ld) + (it - h * V4));
+      }
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int it = i0 + g * nt, h = it / V4, c = it - h * V4;
+        if (it < n && expand[h]) {
+          dense(h, 4 * c, xs[g].x);
+          dense(h, 4 * c + 1, xs[g].y);
+          dense(h, 4 * c + 2, xs[g].z);
+          dense(h, 4 * c + 3, xs[g].w);
+        }
+      }
+    }
+  } else {
+    for (int h = 0; h < beam; ++h) {
+      if (!expand[h]) continue;
+      const float *row = lp + (row0 + h) * ld;
+      for (int v = tid; v < V; v += nt) dense(h, v, __ldg(row + v));
     }
   }
   // closure arcs of every expandable slot in one flattened pass (their
@@ -130,7 +166,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
   if (use_boost) {
     int total = 0;
     for (int h = 0; h < beam; ++h) total += s_rec[h].y;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    for (int idx = tid; idx < total; idx += nt) {
       int h = 0, off = idx;
       while (off >= s_rec[h].y) {
         off -= s_rec[h].y;
@@ -146,10 +182,14 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
   }
 }
 
-// k rounds of block-wide argmax over the per-thread list heads.
+// Block top-k in two levels: each warp pops its own top k from its lanes'
+// lists with warp shuffles only, then warp 0 merges the warps' k-lists —
+// two block barriers in total instead of two per round.
 template <int K>
 __device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp, int *s_win, double *s_key,
                                            double *s_am) {
+  (void)s_warp;
+  __shared__ Cand s_wl[kDbMaxWarps * kMaxTopK];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = 0; r < k; ++r) {
     Cand best = list[0];
@@ -158,18 +198,29 @@ __device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp,
       const Cand oc = shfl_cand(best, o);
       if (cand_better(oc, best)) best = oc;
     }
-    if (lane == 0) s_warp[wid] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      Cand b = s_warp[0];
-      for (int w = 1; w < nw; ++w)
-        if (cand_better(s_warp[w], b)) b = s_warp[w];
-      s_win[r] = b.cid;
-      s_key[r] = b.key;
-      s_am[r] = b.am;
+    if (lane == 0) s_wl[wid * k + r] = best;
+    if (best.cid != INT_MAX && list[0].cid == best.cid) list_pop<K>(list);
+  }
+  __syncthreads();
+  if (wid == 0) {
+    Cand l2[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) l2[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+    for (int j = lane; j < nw * k; j += 32) list_insert<K>(l2, s_wl[j]);
+    for (int r = 0; r < k; ++r) {
+      Cand best = l2[0];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const Cand oc = shfl_cand(best, o);
+        if (cand_better(oc, best)) best = oc;
+      }
+      if (lane == 0) {
+        s_win[r] = best.cid;
+        s_key[r] = best.key;
+        s_am[r] = best.am;
+      }
+      if (best.cid != INT_MAX && l2[0].cid == best.cid) list_pop<K>(l2);
     }
-    __syncthreads();
-    if (s_win[r] != INT_MAX && list[0].cid == s_win[r]) list_pop<K>(list);
   }
   __syncthreads();
 }
@@ -178,15 +229,24 @@ __device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp,
 // Every slot's closure record is loaded at once into s_rec (reused by the
 // candidate scan), then all slots' closure tokens in one flattened pass, so
 // the marking costs two dependent round trips whatever the beam width.
+// Barrier over the worker threads [t0, blockDim.x): the whole block when
+// t0 == 0, else named barrier 1 (warp 0 is busy with the pool merge).
+__device__ __forceinline__ void worker_sync(int t0) {
+  if (t0 == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync 1, %0;" ::"r"(int(blockDim.x) - t0) : "memory");
+}
+
 __device__ __forceinline__ void mark_closures(const TableView &t, unsigned *bm, int bm_words, const SBeam &s,
-                                              const bool *expand, int beam, int4 *s_rec) {
-  for (int i = threadIdx.x; i < beam * bm_words; i += blockDim.x) bm[i] = 0u;
-  for (int h = threadIdx.x; h < beam; h += blockDim.x)
-    s_rec[h] = expand[h] ? __ldg(t.clo_rec + s.tree[h]) : make_int4(0, 0, 0, 0);
-  __syncthreads();
+                                              const bool *expand, int beam, int4 *s_rec, int t0 = 0) {
+  const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
+  for (int i = tid; i < beam * bm_words; i += nt) bm[i] = 0u;
+  for (int h = tid; h < beam; h += nt) s_rec[h] = expand[h] ? __ldg(t.clo_rec + s.tree[h]) : make_int4(0, 0, 0, 0);
+  worker_sync(t0);
   int total = 0;
   for (int h = 0; h < beam; ++h) total += s_rec[h].y;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+  for (int idx = tid; idx < total; idx += nt) {
     int h = 0, off = idx;
     while (off >= s_rec[h].y) {
       off -= s_rec[h].y;
@@ -195,7 +255,7 @@ __device__ __forceinline__ void mark_closures(const TableView &t, unsigned *bm, 
     const int tok = __ldg(&t.clo[s_rec[h].x + off].x);
     atomicOr(bm + h * bm_words + (tok >> 5), 1u << (tok & 31));
   }
-  __syncthreads();
+  worker_sync(t0);
 }
 
 __device__ __forceinline__ void setup_root(const TableView &t, bool use_boost, int smem_root, unsigned char *smem,
@@ -242,12 +302,15 @@ __device__ __forceinline__ void write_hyp(const pgpb_beam_hyps &H, int64_t i, do
 }
 
 template <int K, bool kVec>
-__global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
+__global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
+#ifdef PGPB_TBEAM_PROFILE
+  long long tb_last = clock64();
+#endif
   __shared__ SBeam s;
   __shared__ bool s_expand[kMaxTopK];
   __shared__ int4 s_rec[kMaxTopK];
-  __shared__ Cand s_warp[kBeamThreads / 32];
+  __shared__ Cand s_warp[kDbMaxWarps];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
   __shared__ int s_node_base;
@@ -270,6 +333,7 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
   if (threadIdx.x == 0) s_node_base = S.trace.count[b];
   __syncthreads();
 
+  TB_MARK(0);
   // 1. blank extensions -> finished pool, in rank (slot) order (warp 0).
   // Pools of <= 32 entries live in the warp's registers (lane j = entry j,
   // loaded once), so each slot's merge is a ballot instead of a global round
@@ -282,6 +346,8 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
     uint64_t e_hash = 0;
     double e_am = 0.0, e_bo = 0.0;
     int e_node = -1;
+    // every slot's blank log-prob in flight at once (lane h holds slot h's)
+    const float blank_lp = lane < beam ? __ldg(a.lp + (hb + lane) * a.ld + a.blank) : 0.0f;
     if (lane < cnt) {
       e_len = S.pool.len[pb + lane];
       e_hash = S.pool.hash[pb + lane];
@@ -290,8 +356,9 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
       e_node = S.pool.node[pb + lane];
     }
     for (int h = 0; h < beam; ++h) {
+      const float blp = __shfl_sync(kFull, blank_lp, h);
       if (!(s.flags[h] & kValid)) continue;
-      const double am_e = __dadd_rn(s.am[h], static_cast<double>(__ldg(a.lp + (hb + h) * a.ld + a.blank)));
+      const double am_e = __dadd_rn(s.am[h], static_cast<double>(blp));
       const double bo_e = s.boost[h];
       bool eq = false;
       if (lane < cnt && e_len == s.len[h] && e_hash == s.hash[h]) eq = same_tokens(np, nt, e_node, s.node[h]);
@@ -356,16 +423,25 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
     if (lane == 0) S.pool_count[b] = cnt;
   }
 
+  TB_MARK(1);
   if (expand_wave) {
-    // 2. top-beam non-blank expansions -> next wave
+    // 2. top-beam non-blank expansions -> next wave, on warps 1.. while warp
+    // 0 merges the blank extensions (independent work; they meet at the
+    // top-k barrier)
     const int bm_words = (V + 31) >> 5;
-    if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam, s_rec);
+    const int t0 = blockDim.x > 32 ? 32 : 0;
     Cand list[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
-    scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, a.blank, -1, a.lam,
-                             use_boost, s_rec, list);
+    if (int(threadIdx.x) >= t0) {
+      if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam, s_rec, t0);
+      TB_MARK(2);
+      scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, a.blank, -1, a.lam,
+                               use_boost, s_rec, list, t0);
+    }
+    TB_MARK(3);
     block_topk<K>(list, beam, s_warp, s_win, s_key, s_am);
+    TB_MARK(4);
     for (int r = threadIdx.x; r < beam; r += blockDim.x) {
       const int cid = s_win[r];
       const int64_t o = hb + r;
@@ -396,6 +472,7 @@ __global__ void __launch_bounds__(kBeamThreads) tbeam_wave_kernel(TBeamArgs a) {
       const int64_t lim = S.trace.nmax;
       S.trace.count[b] = int(s_node_base + n < lim ? s_node_base + n : lim);
     }
+    TB_MARK(5);
     return;
   }
 
@@ -471,12 +548,12 @@ struct AedArgs {
 };
 
 template <int K, bool kVec>
-__global__ void __launch_bounds__(kBeamThreads) aed_step_kernel(AedArgs a) {
+__global__ void __launch_bounds__(db_threads<K>()) aed_step_kernel(AedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SBeam s;
   __shared__ bool s_expand[kMaxTopK];
   __shared__ int4 s_rec[kMaxTopK];
-  __shared__ Cand s_warp[kBeamThreads / 32];
+  __shared__ Cand s_warp[kDbMaxWarps];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
   __shared__ int s_node_base, s_any;
@@ -589,12 +666,12 @@ static size_t beam_smem(const TableView &t, bool use_boost, int beam, int &smem_
   return bm + (smem_root ? root : 0);
 }
 
-template <typename Fn, typename Args>
+template <int K, typename Fn, typename Args>
 static int launch_beam(Fn fn, const Args &args, size_t smem, int64_t grid, cudaStream_t st) {
   if (smem > 48 * 1024)
     PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  fn<<<static_cast<unsigned>(grid), kBeamThreads, smem, st>>>(args);
+  fn<<<static_cast<unsigned>(grid), db_threads<K>(), smem, st>>>(args);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }
@@ -649,7 +726,8 @@ int pgpb_tbeam_wave(const pgpb_table *table, const float *d_lp, int64_t ld, int6
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int k = state->beam;
 #define PGPB_TB(KK) \
-  return vec ? launch_beam(tbeam_wave_kernel<KK, true>, a, smem, batch, st) : launch_beam(tbeam_wave_kernel<KK, false>, a, smem, batch, st)
+  return vec ? launch_beam<KK>(tbeam_wave_kernel<KK, true>, a, smem, batch, st) \
+             : launch_beam<KK>(tbeam_wave_kernel<KK, false>, a, smem, batch, st)
   if (k <= 4) PGPB_TB(4);
   if (k <= 8) PGPB_TB(8);
   if (k <= 16) PGPB_TB(16);
@@ -680,12 +758,24 @@ int pgpb_aed_step(const pgpb_table *table, const float *d_lp, int64_t ld, int64_
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int k = state->beam;
 #define PGPB_AE(KK) \
-  return vec ? launch_beam(aed_step_kernel<KK, true>, a, smem, batch, st) : launch_beam(aed_step_kernel<KK, false>, a, smem, batch, st)
+  return vec ? launch_beam<KK>(aed_step_kernel<KK, true>, a, smem, batch, st) \
+             : launch_beam<KK>(aed_step_kernel<KK, false>, a, smem, batch, st)
   if (k <= 4) PGPB_AE(4);
   if (k <= 8) PGPB_AE(8);
   if (k <= 16) PGPB_AE(16);
   PGPB_AE(32);
 #undef PGPB_AE
 }
+
+#ifdef PGPB_TBEAM_PROFILE
+int pgpb_debug_tbeam_profile(unsigned long long *h_out, int reset) {
+  cudaMemcpyFromSymbol(h_out, pgpb::g_tb_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(pgpb::g_tb_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 }  // extern "C"

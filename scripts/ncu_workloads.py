@@ -61,3 +61,14 @@ elif what == "label_loop":
     LabelLoopingDecoder(model, tab, pb.DecodeConfig(lam=1.0), c["B"], c["T"], use_graph=False).decode(enc_proj)
 torch.cuda.synchronize()
 print("ok", what)
+if what.startswith("ctc_clean"):
+    sys.path.insert(0, str(ROOT / "scripts"))
+    import ctc_regimes as cr
+
+    tab, V = cr.table()
+    lp = cr.regimes(128, 200, V, dev)["clean"]
+    lam = 0.0 if what.endswith("unboosted") else 1.0
+    for _ in range(3):
+        pb.ctc_greedy_device(lp, None, tab, pb.DecodeConfig(lam=lam), 0)
+    torch.cuda.synchronize()
+    print("ok", what)
