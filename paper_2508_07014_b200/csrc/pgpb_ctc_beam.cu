@@ -32,7 +32,13 @@ namespace pgpb {
 
 namespace {
 
-constexpr int kCbThreads = 256;
+// Threads per CTA by list size (the per-thread top-K lists' registers):
+// 1024 for K <= 4, 512 for K = 8, 256 beyond.
+template <int K>
+constexpr int cb_threads() {
+  return K <= 4 ? 1024 : (K <= 8 ? 512 : 256);
+}
+constexpr int kCbMaxWarps = 32;
 
 __device__ __forceinline__ double logaddexp(double a, double b) {
   if (a == -INFINITY) return b;
@@ -90,13 +96,13 @@ struct CbArgs {
 };
 
 template <int K, bool kVec>
-__global__ void __launch_bounds__(kCbThreads) ctc_beam_kernel(CbArgs a) {
+__global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Slots cur, nxt;
   __shared__ int s_par[kMaxTopK], s_n;
   __shared__ double s_cpb[kMaxTopK], s_cpnb[kMaxTopK], s_tot[kMaxTopK];
   __shared__ int4 s_rec[kMaxTopK];
-  __shared__ Cand s_warp[kCbThreads / 32];
+  __shared__ Cand s_wl[kCbMaxWarps * kMaxTopK];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
   __shared__ int s_nodes;
@@ -213,36 +219,38 @@ __global__ void __launch_bounds__(kCbThreads) ctc_beam_kernel(CbArgs a) {
       Cand list[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
-      for (int h = 0; h < n; ++h) {
-        const double tot = s_tot[h], pb = cur.pb[h], bh = cur.boost[h];
-        const int last = cur.last[h];
-        const float acc = boost ? __int_as_float(s_rec[h].z) : 0.0f;
-        const unsigned *hb = bm + h * Vw, *he = ex + h * Vw;
-        auto consider = [&](int v, float x, double bv) {
-          if (v == a.blank || ((he[v >> 5] >> (v & 31)) & 1u)) return;
-          const double amv = __dadd_rn(v == last ? pb : tot, static_cast<double>(x));
+      {
+        // candidate (h, v): per-prefix values from shared memory
+        auto dense = [&](int h, int v, float x) {
+          if (v == a.blank || ((ex[h * Vw + (v >> 5)] >> (v & 31)) & 1u)) return;
+          double bv;
+          if (boost) {
+            if ((bm[h * Vw + (v >> 5)] >> (v & 31)) & 1u) return;
+            bv = __dadd_rn(cur.boost[h], static_cast<double>(__int_as_float(s_rec[h].z) + root[v]));
+          } else {
+            bv = __dadd_rn(cur.boost[h], 0.0);
+          }
+          const double amv = __dadd_rn(v == cur.last[h] ? cur.pb[h] : s_tot[h], static_cast<double>(x));
           if (amv == -INFINITY) return;
           list_insert<K>(list, Cand{__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, h * V + v});
         };
-        auto dense = [&](int v, float x) {
-          if (boost) {
-            if ((hb[v >> 5] >> (v & 31)) & 1u) return;
-            consider(v, x, __dadd_rn(bh, static_cast<double>(acc + root[v])));
-          } else {
-            consider(v, x, __dadd_rn(bh, 0.0));
-          }
-        };
+        // work items (prefix, float4 chunk) spread over every thread
         if (kVec) {
+          const int V4 = V >> 2, ni = n * V4;
           const float4 *r4 = reinterpret_cast<const float4 *>(row);
-          for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) {
-            const float4 x = r4[i];
-            dense(4 * i, x.x);
-            dense(4 * i + 1, x.y);
-            dense(4 * i + 2, x.z);
-            dense(4 * i + 3, x.w);
+          for (int it = threadIdx.x; it < ni; it += blockDim.x) {
+            const int h = it / V4, c = it - h * V4;
+            const float4 x = r4[c];
+            dense(h, 4 * c, x.x);
+            dense(h, 4 * c + 1, x.y);
+            dense(h, 4 * c + 2, x.z);
+            dense(h, 4 * c + 3, x.w);
           }
         } else {
-          for (int v = threadIdx.x; v < V; v += blockDim.x) dense(v, row[v]);
+          for (int it = threadIdx.x; it < n * V; it += blockDim.x) {
+            const int h = it / V, v = it - h * V;
+            dense(h, v, row[v]);
+          }
         }
       }
       if (boost) {
@@ -267,7 +275,8 @@ __global__ void __launch_bounds__(kCbThreads) ctc_beam_kernel(CbArgs a) {
         const double amj = logaddexp(s_cpb[j], s_cpnb[j]);
         list_insert<K>(list, Cand{__dadd_rn(amj, __dmul_rn(a.lam, cur.boost[j])), amj, kMaxTopK * V + j});
       }
-      // 4. beam rounds of block argmax
+      // 4. top `beam` in two levels: each warp pops its own top from its
+      // lanes' lists (shuffles only), then warp 0 merges the warps' lists
       for (int r = 0; r < beam; ++r) {
         Cand best = list[0];
 #pragma unroll
@@ -275,19 +284,32 @@ __global__ void __launch_bounds__(kCbThreads) ctc_beam_kernel(CbArgs a) {
           const Cand oc = shfl_cand(best, o);
           if (cand_better(oc, best)) best = oc;
         }
-        if (lane == 0) s_warp[wid] = best;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          Cand bb = s_warp[0];
-          for (int w = 1; w < kCbThreads / 32; ++w)
-            if (cand_better(s_warp[w], bb)) bb = s_warp[w];
-          s_win[r] = bb.cid;
-          s_key[r] = bb.key;
-          s_am[r] = bb.am;
-        }
-        __syncthreads();
-        if (s_win[r] != INT_MAX && list[0].cid == s_win[r]) list_pop<K>(list);
+        if (lane == 0) s_wl[wid * beam + r] = best;
+        if (best.cid != INT_MAX && list[0].cid == best.cid) list_pop<K>(list);
       }
+      __syncthreads();
+      if (wid == 0) {
+        Cand l2[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) l2[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+        const int nw = blockDim.x >> 5;
+        for (int j = lane; j < nw * beam; j += 32) list_insert<K>(l2, s_wl[j]);
+        for (int r = 0; r < beam; ++r) {
+          Cand best = l2[0];
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const Cand oc = shfl_cand(best, o);
+            if (cand_better(oc, best)) best = oc;
+          }
+          if (lane == 0) {
+            s_win[r] = best.cid;
+            s_key[r] = best.key;
+            s_am[r] = best.am;
+          }
+          if (best.cid != INT_MAX && l2[0].cid == best.cid) list_pop<K>(l2);
+        }
+      }
+      __syncthreads();
       // 5. the next beam
       if (threadIdx.x < beam) {
         const int r = threadIdx.x;
@@ -438,7 +460,8 @@ extern "C" int pgpb_ctc_beam(const pgpb_table *table, const float *d_lp, int64_t
                                      int(smem)));
   const int64_t cap = int64_t(sm_count(current_device())) * 2;
   const unsigned grid = unsigned(B < cap ? B : cap);
-  fn<<<grid, kCbThreads, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  const int threads = beam <= 4 ? cb_threads<4>() : (beam <= 8 ? cb_threads<8>() : cb_threads<16>());
+  fn<<<grid, threads, smem, static_cast<cudaStream_t>(stream)>>>(a);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }
