@@ -22,7 +22,10 @@ REF = ROOT / "baseline" / "_ref" / "pkg"
 
 pytestmark = pytest.mark.gpu
 
-SUITES = ["test_table.py", "test_backends.py", "test_acceptance.py", "test_decoding.py"]
+# every reference suite that reaches the kernel module (score_batch /
+# ctc_greedy): the table, backend, acceptance and decoder suites, and the
+# CLI suite that decodes through the same calls
+SUITES = ["test_table.py", "test_backends.py", "test_acceptance.py", "test_decoding.py", "test_cli.py"]
 
 
 @pytest.mark.skipif(not (REF / "tests").is_dir(), reason="baseline/_ref/pkg not built (run __graft_entry__.build())")
