@@ -327,7 +327,8 @@ def _max_over_ranks(x, dev, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    on = dev if world == 1 or dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=on)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
@@ -1169,8 +1170,15 @@ def main():
         import torch
         import torch.distributed as dist
 
+        # one rank per GPU over NCCL; PGPB_BENCH_BACKEND=gloo (test only)
+        # runs the multi-rank code path with several ranks sharing GPUs
+        backend = os.environ.get("PGPB_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     out = run_ours(args, rank, world, local)
     if rank == 0:
         print(json.dumps(out), flush=True)
