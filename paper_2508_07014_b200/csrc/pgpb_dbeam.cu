@@ -112,7 +112,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
                                                 int bm_words, const float *lp, int64_t ld, int64_t row0, int V,
                                                 const SBeam &s, const bool *expand, int beam, int skip, int special,
                                                 double lam, bool use_boost, const int4 *s_rec, Cand (&list)[K],
-                                                int t0 = 0) {
+                                                int t0 = 0, bool closure_pass = true) {
   const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
   // candidate (h, v) of token v at log-prob x (per-slot values from shared memory)
   auto dense = [&](int h, int v, float x) {
@@ -163,7 +163,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
   // closure arcs of every expandable slot in one flattened pass (their
   // entry and log-prob loads in flight together instead of slot by slot;
   // s_rec[h] is zero for slots that do not expand)
-  if (use_boost) {
+  if (use_boost && closure_pass) {
     int total = 0;
     for (int h = 0; h < beam; ++h) total += s_rec[h].y;
     for (int idx = tid; idx < total; idx += nt) {
@@ -254,6 +254,38 @@ __device__ __forceinline__ void mark_closures(const TableView &t, unsigned *bm, 
     }
     const int tok = __ldg(&t.clo[s_rec[h].x + off].x);
     atomicOr(bm + h * bm_words + (tok >> 5), 1u << (tok & 31));
+  }
+  worker_sync(t0);
+}
+
+// mark_closures fused with the closure candidates: each thread that loads
+// a closure entry (token, next, score) sets its bitmap bit and scores it
+// right away (the log-prob gather follows the entry load), so the entries
+// are read once; scan_candidates then runs without its closure pass.
+template <int K>
+__device__ __forceinline__ void mark_and_score_closures(const TableView &t, unsigned *bm, int bm_words,
+                                                        const SBeam &s, const bool *expand, int beam, int4 *s_rec,
+                                                        const float *lp, int64_t ld, int64_t row0, int V, int skip,
+                                                        int special, double lam, Cand (&list)[K], int t0 = 0) {
+  const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
+  for (int i = tid; i < beam * bm_words; i += nt) bm[i] = 0u;
+  for (int h = tid; h < beam; h += nt) s_rec[h] = expand[h] ? __ldg(t.clo_rec + s.tree[h]) : make_int4(0, 0, 0, 0);
+  worker_sync(t0);
+  int total = 0;
+  for (int h = 0; h < beam; ++h) total += s_rec[h].y;
+  for (int idx = tid; idx < total; idx += nt) {
+    int h = 0, off = idx;
+    while (off >= s_rec[h].y) {
+      off -= s_rec[h].y;
+      ++h;
+    }
+    const int4 e = __ldg(t.clo + s_rec[h].x + off);
+    atomicOr(bm + h * bm_words + (e.x >> 5), 1u << (e.x & 31));
+    if (e.x == skip || e.x == special) continue;
+    const float x = __ldg(lp + (row0 + h) * ld + e.x);
+    const double amv = __dadd_rn(s.am[h], static_cast<double>(x));
+    const double bv = __dadd_rn(s.boost[h], static_cast<double>(__int_as_float(e.z)));
+    list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + e.x});
   }
   worker_sync(t0);
 }
@@ -434,10 +466,12 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
 #pragma unroll
     for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
     if (int(threadIdx.x) >= t0) {
-      if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam, s_rec, t0);
+      if (use_boost)
+        mark_and_score_closures<K>(tv, bm, bm_words, s, s_expand, beam, s_rec, a.lp, a.ld, hb, V, a.blank, -1, a.lam,
+                                   list, t0);
       TB_MARK(2);
       scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, a.blank, -1, a.lam,
-                               use_boost, s_rec, list, t0);
+                               use_boost, s_rec, list, t0, false);
     }
     TB_MARK(3);
     block_topk<K>(list, beam, s_warp, s_win, s_key, s_am);
@@ -593,12 +627,13 @@ __global__ void __launch_bounds__(db_threads<K>()) aed_step_kernel(AedArgs a) {
     return;
   }
   const int bm_words = (V + 31) >> 5;
-  if (use_boost) mark_closures(tv, bm, bm_words, s, s_expand, beam, s_rec);
   Cand list[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+  if (use_boost)
+    mark_and_score_closures<K>(tv, bm, bm_words, s, s_expand, beam, s_rec, a.lp, a.ld, hb, V, -1, eos, a.lam, list);
   scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, -1, eos, a.lam, use_boost,
-                           s_rec, list);
+                           s_rec, list, 0, false);
   // carried hypotheses (ended or at max_len), ranked unchanged
   for (int h = threadIdx.x; h < beam; h += blockDim.x)
     if ((s.flags[h] & kValid) && !s_expand[h])
