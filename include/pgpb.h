@@ -310,6 +310,11 @@ int pgpb_rnnt_lstm_update(const void *d_E, const int64_t *d_feed, const void *d_
  * on the device (load_table_device).                                        */
 int pgpb_final_bonus(const pgpb_table *table, float *d_out, void *stream);
 
+/* Per state: the fp32 sum of the backoff weights along its chain, in chain
+ * order (_kernels.pyx:59-66) — the unfinished-phrase credit a hypothesis
+ * ending in that state would give back (rollback extension).  out[S] f32.  */
+int pgpb_backoff_total(const pgpb_table *table, float *d_out, void *stream);
+
 /* Per-state maximum of the resolved score row, max_v scores[s, v]
  * (used by the AED eos bump, decoding.py:546-552).  out[S] f32.             */
 int pgpb_row_max(const pgpb_table *table, float *d_out, void *stream);
@@ -423,6 +428,8 @@ typedef struct pgpb_aed_state {
   int32_t max_len;
   int32_t eos;
   int32_t eos_bump;
+  int32_t rollback;         /* extension (no reference counterpart): the eos
+                               step also adds the state's backoff total      */
 } pgpb_aed_state;
 
 int pgpb_aed_step(const pgpb_table *table, const float *d_logprobs, int64_t ld, int64_t batch,
@@ -456,6 +463,7 @@ typedef struct pgpb_aed_greedy_state {
   int32_t *any_active;
   int32_t max_len;
   int32_t eos;
+  int32_t rollback;         /* extension: eos also adds the backoff total    */
 } pgpb_aed_greedy_state;
 
 int pgpb_aed_greedy_step(const pgpb_table *table, const float *d_logprobs, int64_t ld, int64_t batch,

@@ -289,8 +289,12 @@ def ctc_greedy_numpy(lp, blank, table, lam, enabled=True):
     return {"tokens": toks, "am": am, "boost": boost, "trace": trace}
 
 
-def ctc_beam(lp, blank, table, lam, beam, enabled=True):
-    """Prefix beam search, decoding.py:247-343 (R8).  Returns n-best dicts."""
+def ctc_beam(lp, blank, table, lam, beam, enabled=True, rollback=False):
+    """Prefix beam search, decoding.py:247-343 (R8).  Returns n-best dicts.
+
+    rollback=True is an extension with NO reference counterpart (parity
+    unpinned): after the last frame every prefix gets backoff_total(state)
+    added to its boost before the final ranking."""
     use = _active(table, lam, enabled)
     T, V = lp.shape
     # prefix -> [pb, pnb, state, boost, trace]
@@ -337,6 +341,8 @@ def ctc_beam(lp, blank, table, lam, beam, enabled=True):
         ranked = sorted(new.items(), key=lambda kv: (-(_logaddexp(kv[1][0], kv[1][1]) + lam * kv[1][3]),
                                                      -_logaddexp(kv[1][0], kv[1][1]), kv[0]))
         entries = dict(ranked[:beam])
+    if rollback and use and T > 0:
+        entries = {p: [e[0], e[1], e[2], e[3] + backoff_total(table, e[2]), e[4]] for p, e in entries.items()}
     ranked = sorted(entries.items(), key=lambda kv: (-(_logaddexp(kv[1][0], kv[1][1]) + lam * kv[1][3]),
                                                      -_logaddexp(kv[1][0], kv[1][1]), kv[0]))
     return [{"tokens": list(p), "am": _logaddexp(e[0], e[1]), "boost": e[3], "trace": list(e[4])}
@@ -487,8 +493,12 @@ def transducer_beam(step, T, blank, table, lam, beam_size, max_symbols, V, enabl
     return _out(beam, lam, beam_size)
 
 
-def aed_beam(step, table, lam, beam_size, max_len, eos, V, eos_bump=True, enabled=True):
-    """decoding.py:502-587 (R10).  step(prefix_tuple, len) -> f32 row."""
+def aed_beam(step, table, lam, beam_size, max_len, eos, V, eos_bump=True, enabled=True, rollback=False):
+    """decoding.py:502-587 (R10).  step(prefix_tuple, len) -> f32 row.
+
+    rollback=True is an extension with NO reference counterpart (parity
+    unpinned): the eos step's boost also carries backoff_total(state) (the
+    unfinished phrase's credit taken back when the hypothesis ends)."""
     use = _active(table, lam, enabled)
     rank = _rank(lam)
     beam = [_Hyp((), 0.0, 0.0, 0)]
@@ -510,6 +520,8 @@ def aed_beam(step, table, lam, beam_size, max_len, eos, V, eos_bump=True, enable
                         bump = best if best > 0.0 else 0.0
                         if bool(table.is_final[h.state]):
                             bump += float(table.final_score[h.state])
+                    if use and rollback:
+                        bump += backoff_total(table, h.state)
                     cands.append(_Hyp(h.tokens, h.am + lv, h.boost + bump, h.state, h.last, True,
                                       h.trace + ((eos, bump, h.state),)))
                 else:

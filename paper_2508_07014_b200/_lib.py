@@ -75,7 +75,8 @@ class AedState(ctypes.Structure):
     """pgpb_aed_state."""
 
     _fields_ = [("hyps", BeamHyps), ("trace", BeamTrace), ("row_max", c_void_p), ("any_active", c_void_p),
-                ("beam", c_int32), ("max_len", c_int32), ("eos", c_int32), ("eos_bump", c_int32)]
+                ("beam", c_int32), ("max_len", c_int32), ("eos", c_int32), ("eos_bump", c_int32),
+                ("rollback", c_int32)]
 
 
 class AedGreedyState(ctypes.Structure):
@@ -84,7 +85,7 @@ class AedGreedyState(ctypes.Structure):
     _fields_ = [("tree", c_void_p), ("am", c_void_p), ("boost", c_void_p), ("len", c_void_p), ("ended", c_void_p),
                 ("feed", c_void_p), ("tokens", c_void_p), ("deltas", c_void_p), ("states", c_void_p),
                 ("row_max", c_void_p), ("final_bonus", c_void_p), ("any_active", c_void_p),
-                ("max_len", c_int32), ("eos", c_int32)]
+                ("max_len", c_int32), ("eos", c_int32), ("rollback", c_int32)]
 
 
 class CtcBeamOut(ctypes.Structure):
@@ -122,6 +123,7 @@ _SIGS = {
                          _P, _P, _P, _P, _P, c_void_p],
     "pgpb_row_max": [c_void_p, _P, c_void_p],
     "pgpb_final_bonus": [c_void_p, _P, c_void_p],
+    "pgpb_backoff_total": [c_void_p, _P, c_void_p],
     "pgpb_label_loop_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32,
                              POINTER(LabelLoopState), _P, _P, _P, c_void_p],
     "pgpb_label_loop_step_logits": [c_void_p, _P, c_int64, _P, c_int64, c_int32, c_int32, c_double, c_int32,

@@ -222,7 +222,7 @@ class TransducerBeamDecoder:
     """
 
     def __init__(self, model: StatelessTransducerModel, table: ArcTable | None, cfg: DecodeConfig, batch: int,
-                 max_frames: int, *, use_graph: bool = True, rollback: bool = False, device=None,
+                 max_frames: int, *, use_graph: bool = True, rollback: bool | None = None, device=None,
                  fused: bool = True):
         torch = _torch()
         self.torch, self.model, self.table, self.cfg = torch, model, table, cfg
@@ -248,7 +248,7 @@ class TransducerBeamDecoder:
         self.rows = torch.arange(B, device=d)
         self.state = _lib.TBeamState(self.hyps.struct(), self.pool.struct(), self.pool_count.data_ptr(),
                                      self.trace.struct(), self.t.data_ptr(), self.lengths.data_ptr(), K, self.cap,
-                                     self.pool_cap, int(bool(rollback)))
+                                     self.pool_cap, int(bool(cfg.rollback if rollback is None else rollback)))
         self.use_graph = use_graph
         self.fused = fused and model.dtype == torch.bfloat16
         self.z = torch.zeros((B * K, model.J), dtype=model.dtype, device=d)
@@ -338,7 +338,7 @@ class TransducerBeamDecoder:
 
 
 def transducer_beam_batch(model: StatelessTransducerModel, enc, lengths=None, table: ArcTable | None = None,
-                          cfg: DecodeConfig | None = None, *, rollback: bool = False, vocab=None,
+                          cfg: DecodeConfig | None = None, *, rollback: bool | None = None, vocab=None,
                           want_trace: bool = False) -> list:
     """Batched boosted transducer beam search over enc [B,T,D]: per utterance (best, nbest)."""
     cfg = cfg or DecodeConfig()
@@ -487,7 +487,7 @@ class AEDBeamDecoder:
         self.slot_base = (torch.arange(B, device=d, dtype=torch.int64) * K).unsqueeze(1)
         self.state = _lib.AedState(self.hyps.struct(), self.trace.struct(),
                                    row_max.data_ptr() if row_max is not None else None, self.any_active.data_ptr(),
-                                   K, max_len, eos, int(bool(cfg.eos_bump_enabled)))
+                                   K, max_len, eos, int(bool(cfg.eos_bump_enabled)), int(bool(cfg.rollback)))
         self.launches = 0
         self.use_graph, self._warm, self.graphs = use_graph, False, {}
         self.pool = torch.cuda.graph_pool_handle() if use_graph else None
@@ -587,7 +587,8 @@ class AEDGreedyDecoder:
         p = lambda x: None if x is None else x.data_ptr()  # noqa: E731
         self.state = _lib.AedGreedyState(p(self.tree), p(self.am), p(self.boost), p(self.len), p(self.ended),
                                          p(self.feed), p(self.tokens), p(self.deltas), p(self.states),
-                                         p(self._row_max), p(self._final), p(self.any_active), max_len, eos)
+                                         p(self._row_max), p(self._final), p(self.any_active), max_len, eos,
+                                         int(bool(cfg.rollback)))
         self.launches = 0
         self.use_graph, self._warm, self.graphs = use_graph, False, {}
         self.pool = torch.cuda.graph_pool_handle() if use_graph else None
@@ -704,6 +705,9 @@ def ctc_beam_batch(logprobs, lengths=None, table: ArcTable | None = None, cfg: D
     h = {k: v.cpu().numpy() for k, v in o.items()}
     t = {k: v.cpu().numpy() for k, v in tr.items()}
     lam = cfg.lam
+    if cfg.rollback and _boost_active(table, cfg) and T > 0:  # extension: see DecodeConfig.rollback
+        bt = table.device_table(lp.device.index).backoff_total().cpu().numpy()
+        h["boost"] = h["boost"] + bt[h["tree"]].astype(np.float64)
     results = []
     for b in range(B):
         out = []

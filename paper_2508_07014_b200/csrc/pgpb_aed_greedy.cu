@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(kAgThreads) aed_greedy_kernel(AgArgs a) {
       bump = m > 0.0f ? static_cast<double>(m) : 0.0;
       bump = __dadd_rn(bump, static_cast<double>(__ldg(S.final_bonus + st)));
     }
+    if (boost && S.rollback)  // extension: the unfinished phrase's credit goes back at eos
+      bump = __dadd_rn(bump, static_cast<double>(__int_as_float(__ldg(&t.clo_rec[st].z))));
     if (threadIdx.x == 0) {
       const double amv = __dadd_rn(am0, static_cast<double>(__ldg(row + eos)));
       const double bv = __dadd_rn(bo0, bump);

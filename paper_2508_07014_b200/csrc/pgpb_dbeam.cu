@@ -619,6 +619,8 @@ __global__ void __launch_bounds__(db_threads<K>()) aed_step_kernel(AedArgs a) {
       const int4 rec = __ldg(tv.clo_rec + s.tree[h]);
       if (rec.w) bump = __dadd_rn(bump, static_cast<double>(__ldg(tv.final_score + s.tree[h])));
     }
+    if (ex && use_boost && S.rollback)  // extension: the unfinished phrase's credit goes back at eos
+      bump = __dadd_rn(bump, static_cast<double>(__int_as_float(__ldg(&tv.clo_rec[s.tree[h]].z))));
     s.extra[h] = bump;
   }
   __syncthreads();

@@ -387,6 +387,10 @@ __global__ void final_bonus_kernel(TableView t, float *__restrict__ out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < t.num_states) out[s] = __ldg(&t.clo_rec[s].w) ? __ldg(t.final_score + s) : 0.0f;
 }
+__global__ void backoff_total_kernel(TableView t, float *__restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < t.num_states) out[s] = __int_as_float(__ldg(&t.clo_rec[s].z));
+}
 }  // namespace pgpb
 
 extern "C" {
@@ -482,6 +486,15 @@ int pgpb_final_bonus(const pgpb_table *table, float *d_out, void *stream) {
   if (!table || !d_out) return fail(PGPB_EINVAL, "NULL argument");
   const TableView &t = table->view;
   final_bonus_kernel<<<unsigned((t.num_states + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(t, d_out);
+  PGPB_CUDA_TRY(cudaGetLastError());
+  return PGPB_OK;
+}
+
+int pgpb_backoff_total(const pgpb_table *table, float *d_out, void *stream) {
+  using namespace pgpb;
+  if (!table || !d_out) return fail(PGPB_EINVAL, "NULL argument");
+  const TableView &t = table->view;
+  backoff_total_kernel<<<unsigned((t.num_states + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(t, d_out);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }

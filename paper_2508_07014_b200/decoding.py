@@ -47,6 +47,11 @@ class DecodeConfig:
     max_symbols_per_frame: int = 5
     eos_bump_enabled: bool = True
     boost_enabled: bool = True
+    # Extension with no reference counterpart (parity unpinned, off by
+    # default): when a beam hypothesis is finalised (last frame for CTC /
+    # transducer beams, eos for AED) its boost takes back the unfinished
+    # phrase's credit, i.e. adds the state's backoff total.
+    rollback: bool = False
 
     def __post_init__(self):
         if self.lam < 0:
@@ -377,6 +382,13 @@ class _TopK:
         return out
 
 
+def _backoff_totals(table, use: bool, cfg: DecodeConfig):
+    """Per-state backoff totals (host copy) for the rollback extension, or None."""
+    if not (use and cfg.rollback):
+        return None
+    return table.device_table().backoff_total().cpu().numpy()
+
+
 def _rows_to_device(rows: np.ndarray):
     torch = _torch()
     return torch.from_numpy(np.ascontiguousarray(rows, np.float32)).to("cuda", non_blocking=True)
@@ -453,6 +465,10 @@ def ctc_beam_boosted(em: EmissionMatrix, table: ArcTable | None = None, cfg: Dec
             tr = items[h][1].trace + (TraceStep(v, d, nxt),) if want_trace else ()
             new[np_] = _Prefix(NEG_INF, amv, nxt, bov, tr)
         entries = dict(sorted(new.items(), key=rank)[:beam])
+    bt = _backoff_totals(table, use, cfg)
+    if bt is not None and em.num_frames > 0:
+        for e in entries.values():
+            e.boost = e.boost + float(bt[e.state])
     ranked = sorted(entries.items(), key=rank)[:beam]
     nbest = [DecodeResult(list(p), _text(p, vocab), e.am, e.boost, list(e.trace) if want_trace else None)
              for p, e in ranked]
@@ -480,6 +496,7 @@ def transducer_beam_boosted(step: StepModel, num_frames: int, blank_id: int, tab
     lam, beam_size, cap, V = cfg.lam, cfg.beam_size, cfg.max_symbols_per_frame, step.vocab_size
     rank = _rank_key(lam)
     topk = _TopK(table, use, V, lam)
+    bt = _backoff_totals(table, use, cfg)
     beam = [Hypothesis((), 0.0, 0.0, 0)]
     for t in range(num_frames):
         active: dict = {}
@@ -505,6 +522,8 @@ def transducer_beam_boosted(step: StepModel, num_frames: int, blank_id: int, tab
                                trace=h.trace + (TraceStep(v, d, nxt),) if want_trace else ())
                 nxt_active[(c.tokens, k_wave + 1)] = c
             active = nxt_active
+        if bt is not None and t == num_frames - 1:
+            finished = {k: replace(h, boost_score=h.boost_score + float(bt[h.tree_state])) for k, h in finished.items()}
         beam = sorted(finished.values(), key=rank)[:beam_size]
     nbest = _results(beam, lam, beam_size, vocab, want_trace)
     return nbest[0], nbest
@@ -537,6 +556,7 @@ def aed_beam_boosted(step: StepModel, table: ArcTable | None = None, cfg: Decode
     if use and cfg.eos_bump_enabled:  # device arrays: works for ArcTable and DeviceTable alike
         row_max = table.device_table().row_max().cpu().numpy()
         final_bonus = table.device_table().final_bonus().cpu().numpy()
+    bt = _backoff_totals(table, use, cfg)
     beam = [Hypothesis((), 0.0, 0.0, 0)]
     while True:
         active = [h for h in beam if not h.ended and len(h.tokens) < max_len]
@@ -550,6 +570,8 @@ def aed_beam_boosted(step: StepModel, table: ArcTable | None = None, cfg: Decode
                 best = float(row_max[h.tree_state])
                 bump = best if best > 0.0 else 0.0
                 bump += float(final_bonus[h.tree_state])  # 0 unless final (decoding.py:551-552)
+            if bt is not None:
+                bump += float(bt[h.tree_state])
             cands.append(Hypothesis(h.tokens, h.am_score + float(rows[i, eos]), h.boost_score + bump, h.tree_state,
                                     h.last_token, ended=True,
                                     trace=h.trace + (TraceStep(eos, bump, h.tree_state),) if want_trace else ()))

@@ -56,12 +56,13 @@ class _DeviceTable:
         self._keep = None
         self._row_max = None
         self._final = None
+        self._bt = None
         self._destroy = _lib.LIB.pgpb_table_destroy  # survives interpreter teardown
 
     @classmethod
     def _from_handle(cls, handle: int, device: int) -> "_DeviceTable":
         d = cls.__new__(cls)
-        d.handle, d.device, d._keep, d._row_max, d._final = handle, device, None, None, None
+        d.handle, d.device, d._keep, d._row_max, d._final, d._bt = handle, device, None, None, None, None
         d._destroy = _lib.LIB.pgpb_table_destroy
         return d
 
@@ -90,6 +91,17 @@ class _DeviceTable:
             _lib.check(_lib.LIB.pgpb_final_bonus(self.handle, out.data_ptr(), _lib.stream_ptr()))
             self._final = out
         return self._final
+
+    def backoff_total(self):
+        """Per state the fp32 backoff total of its chain (the rollback
+        extension's credit), as a CUDA f32 tensor (cached)."""
+        import torch
+
+        if self._bt is None:
+            out = torch.empty(self.info().num_states, dtype=torch.float32, device=f"cuda:{self.device}")
+            _lib.check(_lib.LIB.pgpb_backoff_total(self.handle, out.data_ptr(), _lib.stream_ptr()))
+            self._bt = out
+        return self._bt
 
     def __del__(self):
         h = getattr(self, "handle", None)

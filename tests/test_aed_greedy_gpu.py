@@ -19,7 +19,7 @@ from oracle import oracle as orc
 pytestmark = pytest.mark.gpu
 
 
-def _replay(out, B, max_len, eos, tab, lam, V, bump=True, which=None):
+def _replay(out, B, max_len, eos, tab, lam, V, bump=True, which=None, rollback=False):
     for b in (range(B) if which is None else which):
         rows = {}
         res = out.nbest[b]
@@ -29,7 +29,8 @@ def _replay(out, B, max_len, eos, tab, lam, V, bump=True, which=None):
             if ended[b] or n >= max_len:
                 continue
             rows[tuple(toks[:n])] = lp[b].copy()
-        exp = orc.aed_beam(lambda p, n: rows[tuple(p)], tab, lam, 1, max_len, eos, V, eos_bump=bump)
+        exp = orc.aed_beam(lambda p, n: rows[tuple(p)], tab, lam, 1, max_len, eos, V, eos_bump=bump,
+                           rollback=rollback)
         g = res_tuple(res)
         e = exp[0]
         assert g["tokens"] == e["tokens"], b
@@ -37,8 +38,10 @@ def _replay(out, B, max_len, eos, tab, lam, V, bump=True, which=None):
         assert g["trace"] == [list(x) for x in e["trace"]], b
 
 
-@pytest.mark.parametrize("lam,max_len,bump", [(1.0, 8, True), (2.5, 6, True), (1.0, 8, False), (0.0, 7, True)])
-def test_aed_greedy_matches_reference_beam1_by_replay(lam, max_len, bump):
+@pytest.mark.parametrize("lam,max_len,bump,rollback", [(1.0, 8, True, False), (2.5, 6, True, False),
+                                                       (1.0, 8, False, False), (0.0, 7, True, False),
+                                                       (1.0, 8, True, True)])
+def test_aed_greedy_matches_reference_beam1_by_replay(lam, max_len, bump, rollback):
     import torch
 
     from paper_2508_07014_b200 import DecodeConfig
@@ -49,11 +52,11 @@ def test_aed_greedy_matches_reference_beam1_by_replay(lam, max_len, bump):
     model = TransformerAEDModel(V, d_model=32, n_layers=2, n_heads=2, d_ff=64, max_len=max_len + 1, seed=1,
                                 eos_id=V - 1, eos_bias=-1.0, eos_ramp=0.5)
     mem = torch.randn((B, 10, 32), device="cuda", generator=torch.Generator("cuda").manual_seed(3))
-    cfg = DecodeConfig(lam=lam, beam_size=1, eos_bump_enabled=bump)
+    cfg = DecodeConfig(lam=lam, beam_size=1, eos_bump_enabled=bump, rollback=rollback)
     dec = AEDGreedyDecoder(model, tab, cfg, B, max_len=max_len, eos=V - 1, poll=1, use_graph=False)
     out = dec.decode(mem, record=True, want_trace=True)
     assert any(r.trace and r.trace[-1].token == V - 1 for r in out.nbest)  # some utterances end on eos
-    _replay(out, B, max_len, V - 1, tab, lam, V, bump)
+    _replay(out, B, max_len, V - 1, tab, lam, V, bump, rollback=rollback)
 
 
 def test_aed_greedy_equals_device_beam_1_and_graphs():

@@ -168,3 +168,36 @@ def test_exhaustive_ctc_beam_lambda_zero():
         assert tuple(best.tokens) == best_key
         for r in nbest[:20]:
             assert r.am_score == pytest.approx(totals[tuple(r.tokens)], abs=1e-6)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_rollback_extension_reference_api_beams(seed):
+    """DecodeConfig(rollback=True): an extension with no reference
+    counterpart (parity unpinned), checked against the oracle's restatement:
+    CTC / transducer beams add the state's backoff total to every hypothesis
+    at the last frame, the AED beam to the eos step."""
+    from paper_2508_07014_b200 import DecodeConfig, EmissionMatrix, TableStepModel, aed_beam_boosted, \
+        ctc_beam_boosted, transducer_beam_boosted
+
+    rng = np.random.default_rng(500 + seed)
+    V = 48
+    tab = product_table(gi.phrase_corpus(rng, V, 150), V)
+    cfg = DecodeConfig(lam=1.0, beam_size=4, max_symbols_per_frame=2, rollback=True)
+    lp = gi.random_emissions(rng, 12, V)
+    _, nb = ctc_beam_boosted(EmissionMatrix(lp, blank_id=0), tab, cfg, want_trace=True)
+    _cmp(nb, orc.ctc_beam(lp, 0, tab, 1.0, 4, rollback=True))
+    rows, default = gi.random_transducer_rows(rng, V)
+    m = TableStepModel(flavor="transducer", default_row=default, rows=rows)
+    step = lambda last, t: rows.get("" if last is None else str(int(last)), default)  # noqa: E731
+    _, nb = transducer_beam_boosted(m, 5, 0, tab, cfg, want_trace=True)
+    _cmp(nb, orc.transducer_beam(step, 5, 0, tab, 1.0, 4, 2, V, rollback=True))
+    arows, adef = gi.random_aed_rows(rng, V)
+    am = TableStepModel(flavor="aed", default_row=adef, rows=arows, eos_id=V - 1)
+    astep = lambda p, n: arows.get(",".join(map(str, p)), adef)  # noqa: E731
+    _, nb = aed_beam_boosted(am, tab, cfg, max_len=4, want_trace=True)
+    _cmp(nb, orc.aed_beam(astep, tab, 1.0, 4, 4, V - 1, V, rollback=True))
+    # rollback actually changes something on this seed set
+    _, plain = ctc_beam_boosted(EmissionMatrix(lp, blank_id=0), tab, DecodeConfig(lam=1.0, beam_size=4),
+                                want_trace=True)
+    assert [r.boost_score for r in plain] != [r.boost_score for r in ctc_beam_boosted(
+        EmissionMatrix(lp, blank_id=0), tab, cfg)[1]] or seed != 0

@@ -97,3 +97,19 @@ def test_ctc_beam_batch_no_table_and_errors():
         ctc_beam_batch(lps, [9, 10, 1], None, DecodeConfig(beam_size=4), blank_id=0)
     with pytest.raises(ValueError):
         ctc_beam_batch(torch.zeros((2, 3, 12)), None, None, DecodeConfig(beam_size=33), blank_id=0)
+
+
+def test_ctc_beam_batch_rollback_extension():
+    """rollback=True (extension, parity unpinned): equal to the oracle's
+    restatement (backoff total added to every prefix after the last frame)."""
+    from paper_2508_07014_b200 import DecodeConfig
+    from paper_2508_07014_b200.beams import ctc_beam_batch
+
+    phrases, V = gi.corpus("p5k_v1024")
+    tab = product_table(phrases, V)
+    rng = np.random.default_rng(44)
+    lps = np.stack([gi.random_emissions(rng, 20, V) for _ in range(4)])
+    out = ctc_beam_batch(lps, None, tab, DecodeConfig(lam=1.0, beam_size=4, rollback=True), blank_id=0,
+                         want_trace=True)
+    for b in range(4):
+        _cmp(out[b][1], orc.ctc_beam(lps[b], 0, tab, 1.0, 4, rollback=True))

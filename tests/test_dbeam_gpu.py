@@ -104,7 +104,7 @@ def test_transducer_device_beam_graph_equals_eager():
         assert [res_tuple(r) for r in x] == [res_tuple(r) for r in y] == [res_tuple(r) for r in z]
 
 
-def _aed_case(lam, beam, max_len, eos_bump=True, B=4, V=40, seed=0):
+def _aed_case(lam, beam, max_len, eos_bump=True, B=4, V=40, seed=0, rollback=False):
     import torch
 
     from paper_2508_07014_b200 import DecodeConfig
@@ -114,7 +114,7 @@ def _aed_case(lam, beam, max_len, eos_bump=True, B=4, V=40, seed=0):
     model = TransformerAEDModel(V, d_model=32, n_layers=2, n_heads=2, d_ff=64, max_len=max_len + 1, seed=seed)
     mem = torch.randn((B, 10, 32), device="cuda", generator=torch.Generator("cuda").manual_seed(seed))
     eos = V - 1
-    cfg = DecodeConfig(lam=lam, beam_size=beam, eos_bump_enabled=eos_bump)
+    cfg = DecodeConfig(lam=lam, beam_size=beam, eos_bump_enabled=eos_bump, rollback=rollback)
     dec = AEDBeamDecoder(model, tab, cfg, B, max_len=max_len, eos=eos, poll=1)
     out = dec.decode(mem, record=True, want_trace=True)
     for b in range(B):
@@ -128,7 +128,8 @@ def _aed_case(lam, beam, max_len, eos_bump=True, B=4, V=40, seed=0):
                     if prefix in rows:
                         assert np.array_equal(rows[prefix].view(np.uint32), lp[b, r].view(np.uint32))
                     rows[prefix] = lp[b, r].copy()
-        exp = orc.aed_beam(lambda p, n: rows[tuple(p)], tab, lam, beam, max_len, eos, V, eos_bump=eos_bump)
+        exp = orc.aed_beam(lambda p, n: rows[tuple(p)], tab, lam, beam, max_len, eos, V, eos_bump=eos_bump,
+                           rollback=rollback)
         _cmp(out.nbest[b], exp)
 
 
@@ -136,6 +137,13 @@ def _aed_case(lam, beam, max_len, eos_bump=True, B=4, V=40, seed=0):
                                                    (0.0, 4, 5, True), (1.0, 8, 4, True)])
 def test_aed_device_beam_matches_reference_by_replay(lam, beam, max_len, bump):
     _aed_case(lam, beam, max_len, bump)
+
+
+@pytest.mark.parametrize("bump", [True, False])
+def test_aed_device_beam_rollback_extension(bump):
+    """rollback=True (extension, parity unpinned): the eos step also takes
+    back the state's backoff total; equal to the oracle's restatement."""
+    _aed_case(1.0, 4, 6, bump, seed=4, rollback=True)
 
 
 def test_device_beam_rejects_bad_config():
