@@ -411,6 +411,18 @@ int pgpb_tbeam_wave(const pgpb_table *table, const float *d_logprobs, int64_t ld
                     int32_t vocab_size, int32_t blank, double lam, int32_t use_boost, int32_t wave,
                     const pgpb_tbeam_state *state, void *stream);
 
+/* The same wave with the stateless joint's tail fused in: d_logits_bf16
+ * [batch*beam, V] (row stride ld_logits) are log-softmaxed in the kernel
+ * (written to d_lp_out, stride ld: the rows the wave decided on), and the
+ * next wave's joint hidden rows z[b*beam + k] = relu(enc_proj[b, t_b] +
+ * pred_j[last_k]) (bf16, J wide; enc_proj [batch, T, J] with utterance
+ * stride enc_ld_b; pred_j [V, J]) are written to d_z_out at the end — one
+ * kernel instead of three per wave (beams.TransducerBeamDecoder).          */
+int pgpb_tbeam_wave_fused(const pgpb_table *table, const void *d_logits_bf16, int64_t ld_logits, float *d_lp_out,
+                          int64_t ld, int64_t batch, int32_t vocab_size, int32_t blank, double lam,
+                          int32_t use_boost, int32_t wave, const pgpb_tbeam_state *state, const void *d_enc_proj,
+                          int64_t enc_ld_b, int32_t J, const void *d_pred_j, void *d_z_out, void *stream);
+
 /* AED beam step (R10, decoding.py:532-584): candidates are the beam's
  * ended / length-capped hypotheses (carried unchanged) plus every token
  * expansion of the others; eos ends a hypothesis with

@@ -136,6 +136,8 @@ _SIGS = {
                        _P, _P, _P, c_double, c_int32, c_int32, _P, _P, _P, _P, _P, _P, c_void_p],
     "pgpb_tbeam_wave": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32, c_int32,
                         POINTER(TBeamState), c_void_p],
+    "pgpb_tbeam_wave_fused": [c_void_p, _P, c_int64, _P, c_int64, c_int64, c_int32, c_int32, c_double, c_int32,
+                              c_int32, POINTER(TBeamState), _P, c_int64, c_int32, _P, _P, c_void_p],
     "pgpb_phrase_hits": [c_void_p, _P, _P, c_int64, _P, _P, _P, _P, _P, _P, c_void_p],
     "pgpb_aed_step": [c_void_p, _P, c_int64, c_int64, c_int32, c_double, c_int32, POINTER(AedState), c_void_p],
     "pgpb_ctc_beam": [c_void_p, _P, c_int64, c_int64, c_int32, _P, c_int32, c_int32, c_double, c_int32,

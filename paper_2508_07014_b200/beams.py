@@ -255,19 +255,27 @@ class TransducerBeamDecoder:
         self.graph = None
         self.launches = 0
 
+    def _hidden(self):
+        """Joint hidden rows of the current beam (frame gather + context
+        gather + add + ReLU); later waves get them from the fused wave."""
+        m = self.model
+        _lib.check(_lib.LIB.pgpb_rnnt_beam_hidden(
+            self.enc_proj.data_ptr(), self.T * m.J, m.J, self.t.data_ptr(), self.lengths.data_ptr(),
+            m.pred_j.data_ptr(), self.hyps.last.data_ptr(), self.B, self.K, m.blank_id, self.z.data_ptr(),
+            _lib.stream_ptr()), "pgpb_rnnt_beam_hidden")
+
     def _wave(self, k: int):
         torch, m = self.torch, self.model
         if self.fused:
-            # joint as 1 GEMM + 2 kernels: frame gather + context gather + add
-            # + ReLU, the output GEMM, log-softmax (bf16 -> fp32 into self.lp)
-            _lib.check(_lib.LIB.pgpb_rnnt_beam_hidden(
-                self.enc_proj.data_ptr(), self.T * m.J, m.J, self.t.data_ptr(), self.lengths.data_ptr(),
-                m.pred_j.data_ptr(), self.hyps.last.data_ptr(), self.B, self.K, m.blank_id, self.z.data_ptr(),
-                _lib.stream_ptr()), "pgpb_rnnt_beam_hidden")
+            # a wave = the output GEMM + one kernel: log-softmax of the slots'
+            # logits, the wave itself and the next wave's joint hidden rows
             logits = torch.addmm(m.b_out, self.z, m.w_out.T)
-            _lib.check(_lib.LIB.pgpb_log_softmax_bf16(logits.data_ptr(), self.V, self.lp.data_ptr(), self.V,
-                                                      self.B * self.K, self.V, _lib.stream_ptr()),
-                       "pgpb_log_softmax_bf16")
+            _lib.check(_lib.LIB.pgpb_tbeam_wave_fused(
+                self.handle, logits.data_ptr(), self.V, self.lp.data_ptr(), self.V, self.B, self.V, m.blank_id,
+                float(self.cfg.lam), int(self.use), k, _lib.ctypes.byref(self.state), self.enc_proj.data_ptr(),
+                self.T * m.J, m.J, m.pred_j.data_ptr(), self.z.data_ptr(), _lib.stream_ptr()),
+                "pgpb_tbeam_wave_fused")
+            return
         else:
             tf = torch.minimum(self.t, (self.lengths - 1).clamp(min=0)).long()
             self.lp.copy_(m.joint_logprobs(self.enc_proj[self.rows, tf], self.hyps.last))
@@ -316,6 +324,8 @@ class TransducerBeamDecoder:
             self._reset(enc_proj, lengths)
             self._capture()
         self._reset(enc_proj, lengths)
+        if self.fused:
+            self._hidden()  # frame 0, wave 0 (later waves: the fused kernel)
         n_frames = int(self.lengths.max().item()) if self.B else 0
         records = [] if record else None
         for _ in range(n_frames):

@@ -21,6 +21,8 @@
 
 #include <string>
 
+#include <cuda_bf16.h>
+
 #include "pgpb_beam.cuh"
 
 namespace pgpb {
@@ -140,7 +142,8 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         const int it = i0 + g * nt, h = it / V4;
-        if (it < n && expand[h]) xs[g] = __ldg(reinterpret_cast<const float4 *>(lp + (row0 + h) * ld) + (it - h * V4));
+        // generic loads: the rows are global (caller's) or shared (fused log-softmax)
+        if (it < n && expand[h]) xs[g] = reinterpret_cast<const float4 *>(lp + (row0 + h) * ld)[it - h * V4];
       }
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -157,7 +160,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
     for (int h = 0; h < beam; ++h) {
       if (!expand[h]) continue;
       const float *row = lp + (row0 + h) * ld;
-      for (int v = tid; v < V; v += nt) dense(h, v, __ldg(row + v));
+      for (int v = tid; v < V; v += nt) dense(h, v, row[v]);
     }
   }
   // closure arcs of every expandable slot in one flattened pass (their
@@ -174,7 +177,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
       }
       const int4 e = __ldg(t.clo + s_rec[h].x + off);
       if (e.x == skip || e.x == special) continue;
-      const float x = __ldg(lp + (row0 + h) * ld + e.x);
+      const float x = lp[(row0 + h) * ld + e.x];
       const double amv = __dadd_rn(s.am[h], static_cast<double>(x));
       const double bv = __dadd_rn(s.boost[h], static_cast<double>(__int_as_float(e.z)));
       list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + e.x});
@@ -282,7 +285,7 @@ __device__ __forceinline__ void mark_and_score_closures(const TableView &t, unsi
     const int4 e = __ldg(t.clo + s_rec[h].x + off);
     atomicOr(bm + h * bm_words + (e.x >> 5), 1u << (e.x & 31));
     if (e.x == skip || e.x == special) continue;
-    const float x = __ldg(lp + (row0 + h) * ld + e.x);
+    const float x = lp[(row0 + h) * ld + e.x];
     const double amv = __dadd_rn(s.am[h], static_cast<double>(x));
     const double bv = __dadd_rn(s.boost[h], static_cast<double>(__int_as_float(e.z)));
     list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + e.x});
@@ -319,6 +322,17 @@ struct TBeamArgs {
   int wave;
   int smem_root;
   pgpb_tbeam_state s;
+  // fused joint tail (pgpb_tbeam_wave_fused): the slots' bf16 logits are
+  // log-softmaxed here (rows kept in shared memory, written to lp as the
+  // record of what was decided on), and the next wave's joint hidden rows
+  // z = relu(enc_proj[b, t] + pred_j[last]) are written at the end
+  const __nv_bfloat16 *logits;
+  int64_t ld_logits;
+  const __nv_bfloat16 *enc;
+  int64_t enc_ld_b;
+  int J;
+  const __nv_bfloat16 *pred_j;
+  __nv_bfloat16 *z;
 };
 
 __device__ __forceinline__ void write_hyp(const pgpb_beam_hyps &H, int64_t i, double am, double boost, int tree,
@@ -331,6 +345,30 @@ __device__ __forceinline__ void write_hyp(const pgpb_beam_hyps &H, int64_t i, do
   H.len[i] = len;
   H.hash[i] = hash;
   H.flags[i] = flags;
+}
+
+// Fused epilogue: the next wave's joint hidden rows of utterance b's slots,
+// z[b*K + k] = relu(bf16(enc_proj[b, min(t, len-1)] + pred_j[ctx_k])), ctx
+// = the slot's last token (blank at the start), as beam_hidden_kernel.  The
+// hypotheses and t were just written by this block (visible after the
+// barrier; read through L2).
+__device__ __forceinline__ void tbeam_joint_hidden(const TBeamArgs &a, int b, int64_t hb, int beam) {
+  __syncthreads();
+  const pgpb_tbeam_state &S = a.s;
+  const int len = S.lengths[b];
+  int tf = __ldcg(S.t + b);
+  const int lim = len > 0 ? len - 1 : 0;
+  if (tf > lim) tf = lim;
+  const int J = a.J;
+  const __nv_bfloat16 *e = a.enc + int64_t(b) * a.enc_ld_b + int64_t(tf) * J;
+  for (int i = threadIdx.x; i < beam * J; i += blockDim.x) {
+    const int k = i / J, j = i - k * J;
+    const int lst = __ldcg(S.hyps.last + hb + k);
+    const int ctx = lst < 0 ? a.blank : lst;
+    const float sv = __bfloat162float(__float2bfloat16_rn(__bfloat162float(e[j]) +
+                                                          __bfloat162float(a.pred_j[int64_t(ctx) * J + j])));
+    a.z[(hb + k) * J + j] = __float2bfloat16_rn(sv > 0.0f ? sv : 0.0f);
+  }
 }
 
 template <int K, bool kVec>
@@ -359,6 +397,39 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
   const float *root;
   unsigned *bm;
   setup_root(tv, use_boost, a.smem_root, smem, root, bm);
+  // log-prob rows of the beam slots: the caller's f32 rows, or (fused) the
+  // slots' logits log-softmaxed into shared memory after the bitmaps, one
+  // warp per row, torch's formula order (as log_softmax_bf16_kernel)
+  const float *LP = a.lp;
+  int64_t LD = a.ld, R0 = hb;
+  if (a.logits) {
+    const int Vp4 = (V + 3) & ~3;
+    float *lrows = reinterpret_cast<float *>(
+        (reinterpret_cast<uintptr_t>(bm + size_t(beam) * ((V + 31) >> 5)) + 15) & ~uintptr_t(15));
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int r = threadIdx.x >> 5; r < beam; r += nw) {
+      const __nv_bfloat16 *xr = a.logits + (hb + r) * a.ld_logits;
+      float *yr = lrows + size_t(r) * Vp4;
+      float *gr = const_cast<float *>(a.lp) + (hb + r) * a.ld;
+      float m = -INFINITY;
+      for (int v = lane; v < V; v += 32) m = fmaxf(m, __bfloat162float(xr[v]));
+      float mr;
+      asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(m));
+      float sm = 0.0f;
+      for (int v = lane; v < V; v += 32) sm += expf(__bfloat162float(xr[v]) - mr);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(kFull, sm, o);
+      const float ls = logf(sm);
+      for (int v = lane; v < V; v += 32) {
+        const float y = (__bfloat162float(xr[v]) - mr) - ls;
+        yr[v] = y;
+        gr[v] = y;
+      }
+    }
+    LP = lrows;
+    LD = Vp4;
+    R0 = 0;
+  }
   stage_beam(S.hyps, hb, beam, s);
   const bool expand_wave = a.wave < S.cap;
   for (int h = threadIdx.x; h < beam; h += blockDim.x) s_expand[h] = expand_wave && (s.flags[h] & kValid);
@@ -379,7 +450,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     double e_am = 0.0, e_bo = 0.0;
     int e_node = -1;
     // every slot's blank log-prob in flight at once (lane h holds slot h's)
-    const float blank_lp = lane < beam ? __ldg(a.lp + (hb + lane) * a.ld + a.blank) : 0.0f;
+    const float blank_lp = lane < beam ? LP[(R0 + lane) * LD + a.blank] : 0.0f;
     if (lane < cnt) {
       e_len = S.pool.len[pb + lane];
       e_hash = S.pool.hash[pb + lane];
@@ -425,7 +496,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     int cnt = S.pool_count[b];
     for (int h = 0; h < beam; ++h) {
       if (!(s.flags[h] & kValid)) continue;
-      const double am_e = __dadd_rn(s.am[h], static_cast<double>(__ldg(a.lp + (hb + h) * a.ld + a.blank)));
+      const double am_e = __dadd_rn(s.am[h], static_cast<double>(LP[(R0 + h) * LD + a.blank]));
       const double bo_e = s.boost[h];
       int match = -1;
       for (int j0 = 0; j0 < cnt && match < 0; j0 += 32) {
@@ -467,10 +538,10 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
     if (int(threadIdx.x) >= t0) {
       if (use_boost)
-        mark_and_score_closures<K>(tv, bm, bm_words, s, s_expand, beam, s_rec, a.lp, a.ld, hb, V, a.blank, -1, a.lam,
+        mark_and_score_closures<K>(tv, bm, bm_words, s, s_expand, beam, s_rec, LP, LD, R0, V, a.blank, -1, a.lam,
                                    list, t0);
       TB_MARK(2);
-      scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, a.blank, -1, a.lam,
+      scan_candidates<K, kVec>(tv, root, bm, bm_words, LP, LD, R0, V, s, s_expand, beam, a.blank, -1, a.lam,
                                use_boost, s_rec, list, t0, false);
     }
     TB_MARK(3);
@@ -507,6 +578,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
       S.trace.count[b] = int(s_node_base + n < lim ? s_node_base + n : lim);
     }
     TB_MARK(5);
+    if (a.z) tbeam_joint_hidden(a, b, hb, beam);
     return;
   }
 
@@ -565,6 +637,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
       S.t[b] = t + 1;
     }
   }
+  if (a.z) tbeam_joint_hidden(a, b, hb, beam);
 }
 
 // ---------------------------------------------------------------------------
@@ -760,6 +833,59 @@ int pgpb_tbeam_wave(const pgpb_table *table, const float *d_lp, int64_t ld, int6
   a.s = *state;
   const size_t smem = beam_smem(a.t, use_boost, state->beam, a.smem_root);
   const bool vec = (V % 4) == 0 && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(d_lp) % 16) == 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int k = state->beam;
+#define PGPB_TB(KK) \
+  return vec ? launch_beam<KK>(tbeam_wave_kernel<KK, true>, a, smem, batch, st) \
+             : launch_beam<KK>(tbeam_wave_kernel<KK, false>, a, smem, batch, st)
+  if (k <= 4) PGPB_TB(4);
+  if (k <= 8) PGPB_TB(8);
+  if (k <= 16) PGPB_TB(16);
+  PGPB_TB(32);
+#undef PGPB_TB
+}
+
+int pgpb_tbeam_wave_fused(const pgpb_table *table, const void *d_logits_bf16, int64_t ld_logits, float *d_lp_out,
+                          int64_t ld, int64_t batch, int32_t V, int32_t blank, double lam, int32_t use_boost,
+                          int32_t wave, const pgpb_tbeam_state *state, const void *d_enc_proj, int64_t enc_ld_b,
+                          int32_t J, const void *d_pred_j, void *d_z_out, void *stream) {
+  using namespace pgpb;
+  if (!state || !d_logits_bf16 || !d_lp_out || !d_enc_proj || !d_pred_j || !d_z_out)
+    return fail(PGPB_EINVAL, "NULL argument");
+  int rc = check_common(table, ld, batch, V, state->beam, use_boost);
+  if (rc) return rc;
+  if (ld_logits < V || J < 1 || enc_ld_b < J) return fail(PGPB_EINVAL, "bad shape");
+  if (blank < 0 || blank >= V) return fail(PGPB_EINVAL, "blank out of range");
+  if (wave < 0 || wave > state->cap || state->cap < 1) return fail(PGPB_EINVAL, "bad wave index");
+  if (state->pool_cap < state->beam * (state->cap + 1) || state->pool_cap > 64 * 32)
+    return fail(PGPB_EINVAL, "pool_cap must be in [beam*(cap+1), 2048]");
+  if (batch == 0) return PGPB_OK;
+  TBeamArgs a{};
+  a.t = view_or_empty(table, V);
+  a.lp = d_lp_out;
+  a.ld = ld;
+  a.V = V;
+  a.blank = blank;
+  a.lam = lam;
+  a.use_boost = use_boost ? 1 : 0;
+  a.wave = wave;
+  a.s = *state;
+  a.logits = static_cast<const __nv_bfloat16 *>(d_logits_bf16);
+  a.ld_logits = ld_logits;
+  a.enc = static_cast<const __nv_bfloat16 *>(d_enc_proj);
+  a.enc_ld_b = enc_ld_b;
+  a.J = J;
+  a.pred_j = static_cast<const __nv_bfloat16 *>(d_pred_j);
+  a.z = static_cast<__nv_bfloat16 *>(d_z_out);
+  // shared memory: root row | bitmaps (always, the rows follow them) | rows
+  int smem_root = 0;
+  beam_smem(a.t, use_boost, state->beam, smem_root);
+  a.smem_root = smem_root;
+  const size_t bm_bytes = size_t(state->beam) * size_t((V + 31) >> 5) * 4;
+  const size_t smem = (smem_root ? size_t(a.t.vocab_padded) * 4 : 0) + bm_bytes + 16 +
+                      size_t(state->beam) * size_t((V + 3) & ~3) * 4;
+  if (smem > 200 * 1024) return fail(PGPB_EINVAL, "beam x vocabulary too large for the fused wave");
+  const bool vec = (V % 4) == 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int k = state->beam;
 #define PGPB_TB(KK) \
