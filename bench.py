@@ -270,7 +270,8 @@ def run_ours(args, rank, world, local):
                 "d2h_bytes_per_step": R * B * V * 8,
                 "api": "R x paper_2508_07014_b200.get_scores_batch(numpy) -> C-ABI pgpb_advance_host, "
                        "successor gathered on the host",
-                "final_states_match_device_chain": e2e_ok},
+                "final_states_match_device_chain": e2e_ok,
+                **_pcie_roofline(dev, B * V * 8, R * B * V * 8 * e2e_steps / e2e_max / 1e9)},
         "gpu_launches": args.steps + e2e_steps * R,
         "clocks": clk,
     }
@@ -321,6 +322,27 @@ def decode_summary(out):
             d[k] = {"unboosted_ms": round(v["unboosted"]["ms"], 4), "boosted_ms": round(v["boosted"]["ms"], 4),
                     "overhead": round(v["overhead"], 4)}
     return d
+
+
+def _pcie_roofline(dev, nbytes, achieved_gbs):
+    """The e2e path's bound: device-to-host bandwidth of a plain pinned copy
+    of one advance's outputs (nbytes), measured here, against the D2H rate
+    the e2e loop achieved."""
+    import torch
+
+    src = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+    dst = torch.empty(nbytes // 4, dtype=torch.float32, pin_memory=True)
+    dst.copy_(src)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    n = 5
+    for _ in range(n):
+        dst.copy_(src)
+    torch.cuda.synchronize(dev)
+    gbs = nbytes * n / (time.perf_counter() - t0) / 1e9
+    del src, dst
+    return {"d2h_GBps_achieved": achieved_gbs, "d2h_GBps_pinned_copy": gbs, "pcie_frac": achieved_gbs / gbs,
+            "bound": "PCIe D2H of the [B, V] outputs the reference API returns"}
 
 
 def _max_over_ranks(x, dev, world):
