@@ -199,13 +199,15 @@ __device__ __forceinline__ void bcand_consider(BCand &b, double c, float x, int 
   if (rerank_better(c, x, v, b.c, b.lp, b.v)) b = BCand{c, x, v, s, nx, noff};
 }
 
-// Order-preserving unsigned keys for IEEE values (NaN excluded).
+// Order-preserving unsigned keys for IEEE values (NaN excluded).  -0.0 is
+// folded onto +0.0 (x + 0 under round-to-nearest) so the keys order
+// exactly as the reference's float compares, which call them equal.
 __device__ __forceinline__ unsigned long long dkey(double x) {
-  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(x, 0.0)));
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 __device__ __forceinline__ unsigned fkey(float x) {
-  const unsigned u = __float_as_uint(x);
+  const unsigned u = __float_as_uint(__fadd_rn(x, 0.0f));
   return (u >> 31) ? ~u : (u | 0x80000000u);
 }
 
