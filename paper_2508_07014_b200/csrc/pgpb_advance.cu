@@ -4,9 +4,11 @@
 // HBM-write-bound (8 B written per cell).  Kernels:
 //  * advance_v6_kernel: one launch = one advance (pgpb_advance), single-pass
 //    full-line stores with closure overrides patched in by bitmap rank;
-//  * advance_steps_kernel: R chained advances per launch (config 5,
+//  * advance_steps_compact_kernel: R chained advances per launch (config 5,
 //    pgpb_advance_steps), rows split into column parts so small batches
-//    fill the GPU, next-step operands prefetched behind the stores;
+//    fill the GPU, next-step operands prefetched behind the stores, reading
+//    the table's compact advance arrays (V <= 1024);
+//  * advance_steps_kernel: the same on the ranked bitmap rows (any V);
 //  * advance_closure_kernel: generic fallback (any V, unaligned outputs);
 //  * advance_chain_kernel: the reference's chain walk (pgpb_advance_chain),
 //    a cross-check that does not use the flattened closure.
@@ -467,6 +469,119 @@ __global__ void __launch_bounds__(kThreads, 4)
   if (!triggered) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// advance_steps_kernel on the compact arrays (t.adv_bits, V <= 1024): the
+// warp loads the state's whole bitmap line (lane l = word l) and derives
+// each word's rank with an exclusive popc scan, so the successor's token
+// word comes from registers and the closure entries are 8-byte
+// {next, score} pairs: about half the table bytes per random row.
+__device__ __forceinline__ unsigned excl_popc_scan(unsigned w, int lane) {
+  const unsigned c = __popc(w);
+  unsigned x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  return x - c;
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+    advance_steps_compact_kernel(TableView t, const int32_t *__restrict__ states, const int32_t *__restrict__ tokens,
+                                 int R, int64_t B, int P, float *__restrict__ scores, int32_t *__restrict__ next,
+                                 int32_t *__restrict__ trace, int32_t *__restrict__ final_states) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int V = t.vocab_size, Vp = t.vocab_padded, Vw = t.bits_words;
+  float *s_root = reinterpret_cast<float *>(smem);
+  int32_t *s_next = reinterpret_cast<int32_t *>(smem + size_t(Vp) * 4);
+  stage_root(t, s_root, s_next);
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int W = blockDim.x >> 5;
+  const int64_t G = int64_t(gridDim.x) * W;
+  const int CP = (V >> 2) / P;  // float4 chunks per part (multiple of 32)
+  const float4 *r4 = reinterpret_cast<const float4 *>(s_root);
+  const int4 *q4 = reinterpret_cast<const int4 *>(s_next);
+  const int64_t items = B * P;
+  const int64_t cells = B * int64_t(V);
+  bool triggered = false;
+  for (int64_t it = int64_t(blockIdx.x) * W + (threadIdx.x >> 5); it < items; it += G) {
+    const int64_t b = it / P;
+    const int p = int(it - b * P);
+    const int c0 = p * CP;
+    int s = __ldg(states + b);
+    const int4 r0 = __ldg(t.clo_rec + s);
+    int2 rec = make_int2(r0.x, r0.y);  // {clo_start, clo_count}
+    float acc = __int_as_float(r0.z);
+    unsigned w = lane < Vw ? __ldg(t.adv_bits + int64_t(s) * Vw + lane) : 0u;
+    int tok = tokens ? __ldg(tokens + b) : 0;
+    if (!triggered) {
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      triggered = true;
+    }
+    for (int k = 0; k < R; ++k) {
+      // successor (warp-uniform) first, it heads the dependent chain: the
+      // token's word from registers, its rank by one reduction
+      int sn = s;
+      if (tokens) {
+        const int wt = tok >> 5;
+        const unsigned tw = __shfl_sync(kFull, w, wt);
+        const unsigned tr = __reduce_add_sync(kFull, lane < wt ? unsigned(__popc(w)) : 0u);
+        const unsigned bp = unsigned(tok) & 31u;
+        sn = ((tw >> bp) & 1u) ? __ldg(&t.adv_clo[rec.x + int(tr) + __popc(tw & ((1u << bp) - 1u))].x)
+                               : s_next[tok];
+      }
+      int2 nrec = make_int2(0, 0);
+      float nacc = 0.0f;
+      unsigned nw = 0u;
+      int ntok = 0;
+      if (k + 1 < R) {
+        ntok = __ldg(tokens + int64_t(k + 1) * B + b);
+        const int4 r = __ldg(t.clo_rec + sn);
+        nrec = make_int2(r.x, r.y);
+        nacc = __int_as_float(r.z);
+        if (lane < Vw) nw = __ldg(t.adv_bits + int64_t(sn) * Vw + lane);
+      }
+      // word ranks for the row stream, while the lookahead loads are in flight
+      const unsigned rank = excl_popc_scan(w, lane);
+      const int64_t rowoff = int64_t(k) * cells + b * V;
+      float4 *s4 = reinterpret_cast<float4 *>(scores + rowoff);
+      int4 *n4 = reinterpret_cast<int4 *>(next + rowoff);
+      const int2 *arcs = t.adv_clo + rec.x;
+#pragma unroll 2
+      for (int c = c0 + lane; c < c0 + CP; c += 32) {
+        float4 r = r4[c];
+        int4 qv = q4[c];
+        r.x = acc + r.x;  // fp32 add, operand order as _kernels.pyx:70
+        r.y = acc + r.y;
+        r.z = acc + r.z;
+        r.w = acc + r.w;
+        const unsigned word = __shfl_sync(kFull, w, c >> 3);
+        const int base = int(__shfl_sync(kFull, rank, c >> 3));
+        const int sh = (c & 7) * 4;
+        const unsigned bits = (word >> sh) & 0xFu;
+        if (bits) {
+          int q = base + __popc(word & ((1u << sh) - 1u));
+          if (bits & 1u) { const int2 a = __ldg(arcs + q++); r.x = __int_as_float(a.y); qv.x = a.x; }
+          if (bits & 2u) { const int2 a = __ldg(arcs + q++); r.y = __int_as_float(a.y); qv.y = a.x; }
+          if (bits & 4u) { const int2 a = __ldg(arcs + q++); r.z = __int_as_float(a.y); qv.z = a.x; }
+          if (bits & 8u) { const int2 a = __ldg(arcs + q); r.w = __int_as_float(a.y); qv.w = a.x; }
+        }
+        adv_store(s4 + c, r);
+        adv_store(n4 + c, qv);
+      }
+      if (trace && p == 0 && lane == 0) trace[int64_t(k) * B + b] = s;
+      s = sn;
+      rec = nrec;
+      acc = nacc;
+      w = nw;
+      tok = ntok;
+    }
+    if (final_states && p == 0 && lane == 0) final_states[b] = s;
+  }
+  if (!triggered) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Successor gather for the generic chained path: s'[b] = next[b, tok[b]].
 __global__ void __launch_bounds__(256)
     gather_next_kernel(const int32_t *__restrict__ next, const int32_t *__restrict__ tok, int64_t B, int V,
@@ -621,13 +736,18 @@ static int launch_advance_steps(const pgpb_table *table, const int32_t *d_states
   if (ok) {
     const int64_t items = B * P;
     const int64_t ctas = std::min<int64_t>(int64_t(nsm) * per_sm, (items + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    // the compact arrays when built (V <= 1024): with uniformly random states
+    // 89.0% vs 86.7% of the HBM peak at 8192 rows, 92.8% vs 89.1% at 65536,
+    // equal at 1024 (profiles/r2_summary.md §4); the ranked-bitmap kernel
+    // otherwise (tuning adv.compact = 1 forces it, for its tests)
+    auto fn = (t.adv_bits && tuning().adv_compact != 1) ? advance_steps_compact_kernel : advance_steps_kernel;
     if (root_bytes > 48 * 1024)
-      PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(advance_steps_kernel),
+      PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(root_bytes)));
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = pdl_config(dim3(unsigned(ctas)), dim3(kThreads), root_bytes, st, attr);
-    PGPB_CUDA_TRY(cudaLaunchKernelEx(&cfg, advance_steps_kernel, t, d_states, d_tokens, int(R), B, P, d_scores,
-                                     d_next, d_trace, d_final));
+    PGPB_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, t, d_states, d_tokens, int(R), B, P, d_scores, d_next, d_trace,
+                                     d_final));
     PGPB_CUDA_TRY(cudaGetLastError());
     return PGPB_OK;
   }

@@ -20,6 +20,7 @@ struct Tuning {
   int ctc_segment = 0;    // frames per walker segment
   int ctc_seq = 0;        // 1 = sequential walk, 2 = speculative rounds only
   int ll_warps = 0;       // label-loop step: warps (rows) per CTA
+  int adv_compact = 0;    // chained advance: 0 compact table arrays when built, 1 the ranked-bitmap kernel
 };
 Tuning &tuning();
 
@@ -62,6 +63,13 @@ struct TableView {
   // state's largest closure-arc score (bits of an f32, -inf when empty).
   const uint2 *clo_bits;       // [S][Vw] {bits, closure tokens in words < w}
   int32_t bits_words;          // Vw
+  // Advance-only compact copies (V <= 1024, else NULL): the closure bitmap
+  // as plain words (one 128-byte line per state; a warp derives the ranks
+  // with a popc scan) and the closure entries as {next, bits(score)} pairs
+  // (clo without the token, which the bitmap rank already locates).  They
+  // halve the table bytes a uniformly random row pulls from HBM.
+  const uint32_t *adv_bits;    // [S][Vw]
+  const int2 *adv_clo;         // [C]
 };
 
 }  // namespace pgpb

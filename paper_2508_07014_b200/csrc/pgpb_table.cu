@@ -162,6 +162,13 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
         below += static_cast<uint32_t>(__builtin_popcount(w[2 * k]));
       }
     }
+  // advance-only compact copies (pgpb_internal.h)
+  const bool with_adv = with_bits && Vw <= 32;
+  std::vector<uint32_t> adv_bits(with_adv ? static_cast<size_t>(S) * Vw : 1, 0u);
+  if (with_adv)
+    for (size_t i = 0; i < static_cast<size_t>(S) * Vw; ++i) adv_bits[i] = bits[2 * i];
+  std::vector<int2> adv_clo(clo.size());
+  for (size_t i = 0; i < clo.size(); ++i) adv_clo[i] = make_int2(clo[i].y, clo[i].z);
   std::vector<int32_t> rn_off(static_cast<size_t>(Vp), 0);
   for (int32_t v = 0; v < Vp; ++v) rn_off[v] = boff[root_next[v]];
 
@@ -183,6 +190,8 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   const int64_t o_boff = place(int64_t(S) * 4);
   const int64_t o_rno = place(int64_t(Vp) * 4);
   const int64_t o_bits = place(int64_t(bits.size()) * 4);
+  const int64_t o_abits = place(int64_t(adv_bits.size()) * 4);
+  const int64_t o_aclo = place(int64_t(adv_clo.size()) * 8);
   const int64_t total = off;
 
   int prev_dev = 0;
@@ -206,6 +215,8 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   std::memcpy(staging.data() + o_boff, boff.data(), size_t(S) * 4);
   std::memcpy(staging.data() + o_rno, rn_off.data(), size_t(Vp) * 4);
   std::memcpy(staging.data() + o_bits, bits.data(), bits.size() * 4);
+  std::memcpy(staging.data() + o_abits, adv_bits.data(), adv_bits.size() * 4);
+  std::memcpy(staging.data() + o_aclo, adv_clo.data(), adv_clo.size() * 8);
   e = cudaMemcpy(arena, staging.data(), static_cast<size_t>(total), cudaMemcpyHostToDevice);
   cudaSetDevice(prev_dev);
   if (e != cudaSuccess) {
@@ -254,6 +265,8 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   v.root_next_off = reinterpret_cast<const int32_t *>(arena + o_rno);
   v.clo_bits = with_bits ? reinterpret_cast<const uint2 *>(arena + o_bits) : nullptr;
   v.bits_words = Vw;
+  v.adv_bits = with_adv ? reinterpret_cast<const uint32_t *>(arena + o_abits) : nullptr;
+  v.adv_clo = reinterpret_cast<const int2 *>(arena + o_aclo);
   *out = t;
   return PGPB_OK;
 }

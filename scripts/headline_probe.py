@@ -16,9 +16,11 @@ from paper_2508_07014_b200 import _lib  # noqa: E402
 
 tab, V = bw.table("p20k_v1024")
 dt = tab.device_table(0)
-B, R = 8192, 8
+B, R = (int(sys.argv[1]) if len(sys.argv) > 1 else 8192), 8
 rng = np.random.default_rng(1000)
-for n_in, K, ring in ((50, 50, 2), (1, 50, 2), (50, 20, 2), (20, 20, 2), (50, 50, 3), (50, 50, 4)):
+cases = [(n_in, 50 if B <= 8192 else 8, 2, cm) for cm in (1, 2) for n_in in (50 if B <= 8192 else 8, 1)]
+for n_in, K, ring, cm in cases:
+    _lib.set_tuning("adv.compact", cm)
     st = torch.from_numpy(rng.integers(0, tab.num_states, size=(n_in, B)).astype(np.int32)).cuda()
     tk = torch.from_numpy(rng.integers(0, V, size=(n_in, R, B)).astype(np.int32)).cuda()
     outs = [(torch.empty((R, B, V), dtype=torch.float32, device="cuda"),
@@ -44,6 +46,6 @@ for n_in, K, ring in ((50, 50, 2), (1, 50, 2), (50, 20, 2), (20, 20, 2), (50, 50
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) / K)
     frac = [round(R * (B * V * 8 + B * 4) / (t / 1e3) / 1e9 / 6454.9, 3) for t in ts]
-    print(f"n_in={n_in} K={K} ring={ring} per-replay frac {frac}", flush=True)
+    print(f"n_in={n_in} K={K} ring={ring} layout={cm} per-replay frac {frac}", flush=True)
     del outs, g
     torch.cuda.empty_cache()

@@ -103,7 +103,8 @@ def _closure_biased_tokens(tab, states0, R, rng, p_closure=0.6):
                                             ("p20k_v1024", 300, 5, 2), ("p20k_v1024", 97, 3, 8),
                                             ("p20k_v1024", 8192, 2, 0), ("p20k_v4096", 256, 3, 0),
                                             ("p5k_v1024", 4, 7, 0)])
-def test_advance_steps_vs_oracle(name, B, R, parts):
+@pytest.mark.parametrize("layout", [0, 1])
+def test_advance_steps_vs_oracle(name, B, R, parts, layout):
     """Chained R-step advance (config 5): every step's rows bit-exact vs the
     oracle advance of that step's states, and s_{k+1} = next_k[b, tok_k[b]]."""
     import torch
@@ -118,7 +119,12 @@ def test_advance_steps_vs_oracle(name, B, R, parts):
         toks = _closure_biased_tokens(tab, s0, R, rng)
     else:
         toks = rng.integers(0, V, size=(R, B)).astype(np.int32)
-    r = advance_steps(tab, torch.from_numpy(s0).cuda(), torch.from_numpy(toks).cuda(), parts=parts)
+    from paper_2508_07014_b200 import _lib
+    _lib.set_tuning("adv.compact", layout)  # 0: compact arrays (V <= 1024), 1: the ranked-bitmap kernel
+    try:
+        r = advance_steps(tab, torch.from_numpy(s0).cuda(), torch.from_numpy(toks).cuda(), parts=parts)
+    finally:
+        _lib.set_tuning("adv.compact", 0)
     tr = r.trace.cpu().numpy()
     assert np.array_equal(tr[0], s0)
     s = s0
