@@ -262,7 +262,7 @@ def run_ours(args, rank, world, local):
         "config": config5(world, S, V, len(phrases)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": ncu_traffic(), "peak_kind": peak_kind,
-                     "kernel": "advance_steps_kernel", "bytes_alg_per_launch": bytes_alg,
+                     "kernel": "advance_steps_compact_kernel", "bytes_alg_per_launch": bytes_alg,
                      "bytes_alg_formula": "R x (B*V*8 + B*4): f32 score + i32 next per cell, i32 state per row",
                      "kernel_ms": kern_ms,
                      "timing": "CUDA events around one graph replay of the K back-to-back launches"},
@@ -555,7 +555,7 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
 def bench_advance_sweep(dtab, S, V, dev, hbm_peak, batches=(128, 1024, 8192, 65536), steps=20, R=R_STEPS):
     """SURVEY 8(d) batch sweep of the advance on one GPU, uniform random
     states: `single` = one advance per launch (advance_v6_kernel), `chained`
-    = R chained steps per launch (advance_steps_kernel); K back-to-back
+    = R chained steps per launch (advance_steps_compact_kernel); K back-to-back
     launches in one graph over an output ring larger than L2 (>= 256 MiB);
     device time per launch and the fraction of the measured HBM peak
     (8 B per cell + 4 B per state row)."""

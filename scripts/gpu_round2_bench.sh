@@ -10,7 +10,7 @@ timeout 300 python bench.py --impl reference --steps 5 --warmup 2 > gpurun_out/r
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
   --log-file gpurun_out/r2_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-decode \
   > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:advance_steps_kernel -s 6 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:advance_steps_compact_kernel -s 6 -c 1 \
   -o gpurun_out/r2_advance_steps python bench.py --steps 8 --warmup 3 --no-cpu-baseline --no-decode \
   > gpurun_out/r2_ncu_full.log 2>&1
 tail -3 gpurun_out/r2_ncu_full.log
