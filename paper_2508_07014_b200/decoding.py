@@ -335,7 +335,15 @@ def transducer_greedy_boosted(step: StepModel, num_frames: int, blank_id: int, t
 
 
 class _TopK:
-    """One call of pgpb_beam_topk for a single group of hypotheses."""
+    """pgpb_beam_topk for a single group of hypotheses.
+
+    The device orders candidates by (combined, am, hypothesis, token); the
+    reference ranks equal (combined, am) by token tuple instead
+    (decoding.py:323-327, :407-411).  So that exact ties at the cut cannot
+    change which candidates survive, the result is extended past k by every
+    candidate tied with the k-th (fetched on demand: normally one extra
+    candidate shows there is no tie), and the callers re-rank with the
+    reference's full key before truncating."""
 
     def __init__(self, table, use, V, lam):
         self.torch = _torch()
@@ -344,9 +352,29 @@ class _TopK:
 
     def __call__(self, rows_dev, ld, states, am, boost, exclude, k, alt_token=None, alt_am=None,
                  valid=None, skip_neg_inf=False):
-        torch = self.torch
         H = len(am)
         k = min(int(k), H * self.V)  # never more winners than candidates
+        if k <= 0:
+            return []
+        lam = self.lam
+
+        def tie(a, b):
+            return a[2] == b[2] and a[2] + lam * a[3] == b[2] + lam * b[3]
+
+        kr = min(k + 1, H * self.V)
+        while True:
+            out = self._run(rows_dev, ld, states, am, boost, exclude, kr, alt_token, alt_am, valid, skip_neg_inf)
+            if len(out) <= k or not tie(out[k - 1], out[-1]) or len(out) < kr or kr == H * self.V:
+                break
+            kr = min(2 * kr, H * self.V)  # the tie group may run past what was fetched
+        n = min(k, len(out))
+        while n < len(out) and tie(out[k - 1], out[n]):
+            n += 1
+        return out[:n]
+
+    def _run(self, rows_dev, ld, states, am, boost, exclude, k, alt_token, alt_am, valid, skip_neg_inf):
+        torch = self.torch
+        H = len(am)
         dev = rows_dev.device
 
         def t(x, dt):
@@ -514,8 +542,10 @@ def transducer_beam_boosted(step: StepModel, num_frames: int, blank_id: int, tab
             hyps = [h for _, h in waves]
             cands = topk(_rows_to_device(rows), V, [h.tree_state for h in hyps], [h.am_score for h in hyps],
                          [h.boost_score for h in hyps], [blank_id] * len(hyps), beam_size)
+            # the reference's prune order, token tuples breaking exact ties (decoding.py:490)
+            cands = sorted(cands, key=lambda c: (-(c[2] + lam * c[3]), -c[2], hyps[c[0]].tokens + (c[1],)))
             nxt_active = {}
-            for hi, v, amv, bov, nxt, delta in cands:
+            for hi, v, amv, bov, nxt, delta in cands[:beam_size]:
                 h = hyps[hi]
                 d = delta if use else 0.0
                 c = Hypothesis(h.tokens + (v,), amv, bov, nxt, v,

@@ -67,6 +67,33 @@ def random_transducer_rows(rng, V):
     return rows, default
 
 
+def tied_rows(rng, n, V):
+    """Rows with exact score ties across hypotheses: integer log-scores in
+    {-4..-1} (the reference does not require normalised rows, and fp64 sums
+    of small integers are exact, so different token sequences reach equal
+    (combined, am) keys), every fourth row uniform (-2)."""
+    z = -rng.integers(1, 5, size=(n, V)).astype(np.float32)
+    z[::4] = -2.0
+    return z
+
+
+def tied_transducer_rows(rng, V):
+    r = tied_rows(rng, V + 2, V)
+    rows = {str(ctx): r[ctx] for ctx in range(V)}
+    rows[""] = r[V]
+    return rows, r[V + 1]
+
+
+def tied_aed_rows(rng, V, n_rows=6):
+    rows = {}
+    r = tied_rows(rng, n_rows + 1, V)
+    for i in range(n_rows):
+        plen = int(rng.integers(0, 3))
+        key = ",".join(str(int(x)) for x in rng.integers(0, V, size=plen))
+        rows[key] = r[i]
+    return rows, r[n_rows]
+
+
 def random_aed_rows(rng, V, n_rows=6):
     rows = {}
     for _ in range(n_rows):
