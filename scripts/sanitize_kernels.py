@@ -27,7 +27,12 @@ r = pb.get_scores_batch(tab, st)
 sc, nx = orc.score_batch(tab, st)
 assert np.array_equal(r.next_states, nx)
 toks = torch.from_numpy(rng.integers(0, V, size=(3, 300)).astype(np.int32)).to(dev)
+pb.advance_steps(tab, torch.from_numpy(st).to(dev), toks)  # compact arrays (V <= 1024)
+from paper_2508_07014_b200 import _lib  # noqa: E402
+
+_lib.set_tuning("adv.compact", 1)  # the ranked-bitmap chained kernel
 pb.advance_steps(tab, torch.from_numpy(st).to(dev), toks)
+_lib.set_tuning("adv.compact", 0)
 from paper_2508_07014_b200.table import _advance_device  # noqa: E402
 
 _advance_device(tab, torch.from_numpy(st).to(dev), check=True, out=None, chain=True)
