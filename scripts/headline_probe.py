@@ -16,9 +16,11 @@ from paper_2508_07014_b200 import _lib  # noqa: E402
 
 tab, V = bw.table("p20k_v1024")
 dt = tab.device_table(0)
-B, R = (int(sys.argv[1]) if len(sys.argv) > 1 else 8192), 8
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+R = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 rng = np.random.default_rng(1000)
-cases = [(n_in, 50 if B <= 8192 else 8, 2, cm) for cm in (1, 2) for n_in in (50 if B <= 8192 else 8, 1)]
+big = B * R > 8192 * 8
+cases = [(n_in, 8 if big else 50, 2, cm) for cm in (1, 2) for n_in in ((8 if big else 50), 1)]
 for n_in, K, ring, cm in cases:
     _lib.set_tuning("adv.compact", cm)
     st = torch.from_numpy(rng.integers(0, tab.num_states, size=(n_in, B)).astype(np.int32)).cuda()
