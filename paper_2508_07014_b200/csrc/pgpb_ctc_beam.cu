@@ -95,13 +95,22 @@ struct CbArgs {
   int32_t *overflow;
 };
 
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
 template <int K, bool kVec>
 __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Slots cur, nxt;
   __shared__ int s_par[kMaxTopK], s_n;
   __shared__ double s_cpb[kMaxTopK], s_cpnb[kMaxTopK], s_tot[kMaxTopK];
-  __shared__ int4 s_rec[kMaxTopK];
+  // closure records of the live prefixes' states, double-buffered: the next
+  // frame's are fetched (cp.async, own commit group) as soon as the winners'
+  // states are known, and waited for only after the next frame's carries
+  __shared__ __align__(16) int4 s_rec2[2][kMaxTopK];
   __shared__ Cand s_wl[kCbMaxWarps * kMaxTopK];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
@@ -140,13 +149,16 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
       s_n = 1;
       s_nodes = 0;
     }
-    // frame 0's row
+    // frame 0's row and the root's closure record
     const float *lpb = a.lp + b * a.T * int64_t(V);
     if (Tb > 0)
       for (int i = threadIdx.x; i < V; i += blockDim.x) rows[i] = __ldg(lpb + i);
+    if (boost && threadIdx.x == 0) cp_async16(&s_rec2[0][0], t.clo_rec);
+    asm volatile("cp.async.commit_group;" ::: "memory");
     __syncthreads();
     for (int64_t tf = 0; tf < Tb; ++tf) {
       const float *row = rows + (tf & 1) * Vp;
+      int4 *s_rec = s_rec2[tf & 1];
       // prefetch the next frame's row into the other buffer (consumed after
       // this frame's barriers)
       if (tf + 1 < Tb) {
@@ -192,10 +204,10 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
       // exclusion bitmaps (extensions landing on a live prefix) and
       // closure records
       for (int i = threadIdx.x; i < n * Vw; i += blockDim.x) ex[i] = 0u;
-      if (boost) {
+      if (boost)
         for (int i = threadIdx.x; i < n * Vw; i += blockDim.x) bm[i] = 0u;
-        for (int h = threadIdx.x; h < n; h += blockDim.x) s_rec[h] = __ldg(t.clo_rec + cur.tree[h]);
-      }
+      // this frame's closure records (issued last frame); the next row may pend
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
       __syncthreads();
       if (threadIdx.x < n && s_par[threadIdx.x] >= 0) {
         const int v = cur.last[threadIdx.x];
@@ -317,6 +329,7 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
         if (cid != INT_MAX) {
           if (cid >= kMaxTopK * V) {  // carried prefix
             const int j = cid - kMaxTopK * V;
+            if (boost) cp_async16(&s_rec2[(tf + 1) & 1][r], t.clo_rec + cur.tree[j]);
             nxt.pb[r] = s_cpb[j];
             nxt.pnb[r] = s_cpnb[j];
             nxt.boost[r] = cur.boost[j];
@@ -330,7 +343,10 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
             const int h = cid / V, v = cid - h * V;
             float sc = 0.0f;
             int nx = 0;
-            if (boost) resolve_ranked(t, root, bm + h * Vw, s_rec[h], v, sc, nx);
+            if (boost) {
+              resolve_ranked(t, root, bm + h * Vw, s_rec[h], v, sc, nx);
+              cp_async16(&s_rec2[(tf + 1) & 1][r], t.clo_rec + nx);
+            }
             // trace node: winners of this frame take consecutive nodes in
             // rank order among the new prefixes
             int rank = 0;
@@ -378,9 +394,12 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
         cur.node[r] = nxt.node[r];
         cur.len[r] = nxt.len[r];
       }
-      if (kVec) asm volatile("cp.async.wait_all;" ::: "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");  // the next frame's records
+      // the next row has landed (the records' group may still pend)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
       __syncthreads();
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     // final beam (rank order)
     if (threadIdx.x < beam) {
       const int r = threadIdx.x;
