@@ -335,7 +335,10 @@ int pgpb_row_max(const pgpb_table *table, float *d_out, void *stream);
  * is -inf are dropped (decoding.py:303-304).  The [H,V] score matrix is
  * never materialised.  Outputs are [G, k]; unfilled slots get hyp = -1.
  * alt_token / alt_am / valid may be NULL.  ld = 0 broadcasts one row to all
- * hypotheses (CTC prefix beam: every prefix reads the same frame).         */
+ * hypotheses (CTC prefix beam: every prefix reads the same frame).  The
+ * reference breaks (key, am) ties by token tuple; the Python drop-in beams
+ * ask for k + 1, extend the cut by the whole tie group and re-rank on the
+ * host with the tuples (decoding._TopK), so their results are exact on ties. */
 int pgpb_beam_topk(const pgpb_table *table, const float *d_logprobs, int64_t ld,
                    int64_t hyps, int32_t vocab_size, int32_t group, int32_t k,
                    const int32_t *d_states, const double *d_am, const double *d_boost,
