@@ -335,6 +335,10 @@ def decode_summary(out):
         if isinstance(v, dict) and "overhead" in v:
             d[f"ctc_greedy_{k}"] = {"unboosted_ms": round(v["unboosted"]["ms"], 5),
                                     "boosted_ms": round(v["boosted"]["ms"], 5), "overhead": round(v["overhead"], 4)}
+    rp = c.get("ref_corpus_25x1800", {}).get("reference_protocol")
+    if rp:
+        d["ctc_greedy_reference_protocol"] = {"base_s": round(rp["base_s"], 5), "boosted_s": round(rp["boosted_s"], 5),
+                                              "overhead": round(rp["overhead"], 4)}
     for k, v in out.get("decode_ctc_beam", {}).items():
         if isinstance(v, dict) and "overhead" in v:
             d[f"ctc_beam_{k}"] = {"unboosted_ms": round(v["unboosted"]["ms"], 4),
@@ -565,13 +569,35 @@ def bench_decode(tab, V, dev, rank, world, B=128, T=200, reps=10):
             res["cpu_reference"] = cpu_ctc_reference(lp[: min(B, 32)].cpu().numpy(), tab, B, T)
         if rank == 0 and regime.startswith("ref_corpus"):
             ln = lens.cpu().numpy()
-            res["cpu_reference"] = cpu_ctc_reference([x[:n] for x, n in zip(lp.cpu().numpy(), ln)], tab,
-                                                     len(ln), float(ln.mean()))
+            host = lp.cpu().numpy()
+            res["cpu_reference"] = cpu_ctc_reference([x[:n] for x, n in zip(host, ln)], tab, len(ln), float(ln.mean()))
+            res["reference_protocol"] = ctc_reference_protocol([x[:n] for x, n in zip(host, ln)], tab)
 
         out[regime] = res
         del lp
     out["_launches"] = launches
     return out
+
+
+def ctc_reference_protocol(utts, tab):
+    """The reference's own decode-overhead criterion (test_acceptance.py:
+    342-378) on this package's drop-in API: per-utterance
+    ctc_greedy_boosted calls on host EmissionMatrix inputs (H2D, fused kernel,
+    D2H per call), lam=0 without a table vs lam=1 with the 20K table, wall
+    clock, evaluation.bench (1 warm-up, mean of 3), outputs compared."""
+    import paper_2508_07014_b200 as pb
+    from paper_2508_07014_b200.acoustic import EmissionMatrix
+    from paper_2508_07014_b200.evaluation import bench as ev_bench
+
+    ems = [EmissionMatrix(np.ascontiguousarray(u), blank_id=0) for u in utts]
+    base = ev_bench(lambda: [pb.ctc_greedy_boosted(em, None, pb.DecodeConfig(lam=0.0)).tokens for em in ems],
+                    runs=3, warmup=1)
+    boosted = ev_bench(lambda: [pb.ctc_greedy_boosted(em, tab, pb.DecodeConfig(lam=1.0)).tokens for em in ems],
+                       runs=3, warmup=1)
+    return {"protocol": "test_acceptance.py:342-378 (25 utterances, per-utterance drop-in calls, wall clock)",
+            "base_s": base.mean_seconds, "boosted_s": boosted.mean_seconds,
+            "overhead": boosted.mean_seconds / base.mean_seconds - 1.0, "reference_bound": 0.15,
+            "boosted_equals_base": boosted.output == base.output}
 
 
 def bench_advance_sweep(dtab, S, V, dev, hbm_peak, batches=(128, 1024, 8192, 65536), steps=20, R=R_SWEEP):
