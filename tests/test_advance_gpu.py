@@ -279,3 +279,32 @@ def test_row_max_matches_oracle():
     idx = np.random.default_rng(3).integers(0, tab.num_states, size=300)
     sc, _ = orc.score_batch(tab, idx.astype(np.int32))
     assert bits_equal(rm[idx], sc.max(axis=1))
+
+
+@pytest.mark.parametrize("V,parts", [(896, 0), (512, 0), (512, 2), (256, 1), (128, 1)])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_advance_steps_split_shapes(V, parts, layout):
+    """Chained kernels at vocabularies below 1024 (compact arrays built, fewer
+    than 32 bitmap words, one or two column parts; V = 896 leaves lanes 28-31
+    without a word), both table layouts, closure-biased token streams."""
+    import torch
+
+    from paper_2508_07014_b200 import _lib, advance_steps
+
+    rng = np.random.default_rng(V * 7 + parts)
+    tab = product_table(gi.random_phrase_set(rng, 300, 8, V), V, unk=-0.1)
+    B, R = 77, 5
+    s0 = rng.integers(0, tab.num_states, size=B).astype(np.int32)
+    toks = _closure_biased_tokens(tab, s0, R, rng)
+    _lib.set_tuning("adv.compact", layout)
+    try:
+        r = advance_steps(tab, torch.from_numpy(s0).cuda(), torch.from_numpy(toks).cuda(), parts=parts)
+    finally:
+        _lib.set_tuning("adv.compact", 0)
+    s = s0
+    for k in range(R):
+        sc, nx = orc.score_batch(tab, s)
+        assert np.array_equal(r.trace[k].cpu().numpy(), s)
+        assert bits_equal(r.scores[k].cpu().numpy(), sc) and np.array_equal(r.next_states[k].cpu().numpy(), nx)
+        s = nx[np.arange(B), toks[k]].astype(np.int32)
+    assert np.array_equal(r.final_states.cpu().numpy(), s)
