@@ -4,10 +4,12 @@
 // HBM-write-bound (8 B written per cell).  Kernels:
 //  * advance_v6_kernel: one launch = one advance (pgpb_advance), single-pass
 //    full-line stores with closure overrides patched in by bitmap rank;
-//  * advance_steps_compact_kernel: R chained advances per launch (config 5,
-//    pgpb_advance_steps), rows split into column parts so small batches
-//    fill the GPU, next-step operands prefetched behind the stores, reading
-//    the table's compact advance arrays (V <= 1024);
+//  * advance_steps_blob_kernel / advance_steps_compact_kernel: R chained
+//    advances per launch (config 5, pgpb_advance_steps), rows split into
+//    column parts so small batches fill the GPU, next-step operands fetched
+//    behind the stores; the first reads per-state advance blobs into shared
+//    memory (latency-bound launches), the second the compact advance arrays
+//    (bandwidth-bound launches); V <= 1024;
 //  * advance_steps_kernel: the same on the ranked bitmap rows (any V);
 //  * advance_closure_kernel: generic fallback (any V, unaligned outputs);
 //  * advance_chain_kernel: the reference's chain walk (pgpb_advance_chain),
@@ -582,6 +584,126 @@ __global__ void __launch_bounds__(kThreads, 4)
   if (!triggered) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// advance_steps on the per-state advance blobs (t.adv_blob): a warp copies
+// the next state's whole blob (closure accumulator, bitmap words, word ranks,
+// {next, score} pairs) into its shared-memory buffer with one 16-B cp.async
+// per lane, one step ahead, so a step resolves its successor, ranks and
+// every override from shared memory: no dependent global load on the step's
+// path (the closure-override loads inside the stream were its largest
+// stall, profiles/r2_summary.md §4).
+__device__ __forceinline__ void adv_cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
+    advance_steps_blob_kernel(TableView t, const int32_t *__restrict__ states, const int32_t *__restrict__ tokens,
+                              int R, int64_t B, int P, float *__restrict__ scores, int32_t *__restrict__ next,
+                              int32_t *__restrict__ trace, int32_t *__restrict__ final_states) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int V = t.vocab_size, Vp = t.vocab_padded, Vw = t.bits_words;
+  const int S16 = t.adv_stride16, E0 = t.adv_ent0;
+  float *s_root = reinterpret_cast<float *>(smem);
+  int32_t *s_next = reinterpret_cast<int32_t *>(smem + size_t(Vp) * 4);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int4 *bufs = reinterpret_cast<int4 *>(smem + size_t(Vp) * 8) + size_t(wid) * 2 * S16;  // 2 blobs per warp
+  // closure counts of the root row's successors (sizes the copy of a dense successor's blob)
+  unsigned char *s_cnt = reinterpret_cast<unsigned char *>(smem + size_t(Vp) * 8 + size_t(blockDim.x >> 5) * 2 * S16 * 16);
+  stage_root(t, s_root, s_next);
+  __syncthreads();
+  for (int v = threadIdx.x; v < V; v += blockDim.x) s_cnt[v] = static_cast<unsigned char>(__ldg(&t.clo_rec[s_next[v]].y));
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int W = blockDim.x >> 5;
+  const int64_t G = int64_t(gridDim.x) * W;
+  const int CP = (V >> 2) / P;
+  const float4 *r4 = reinterpret_cast<const float4 *>(s_root);
+  const int4 *q4 = reinterpret_cast<const int4 *>(s_next);
+  const int64_t items = B * P;
+  const int64_t cells = B * int64_t(V);
+  // copy the used prefix of a blob: header, words, ranks and cnt pairs
+  auto fetch = [&](int st, int cnt, int slot) {
+    const int4 *src = t.adv_blob + int64_t(st) * S16;
+    int4 *dst = bufs + slot * S16;
+    const int n16 = min(S16, (E0 + 2 * cnt + 3) >> 2);
+    for (int i = lane; i < n16; i += 32) adv_cp_async16(dst + i, src + i);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  bool triggered = false;
+  for (int64_t it = int64_t(blockIdx.x) * W + wid; it < items; it += G) {
+    const int64_t b = it / P;
+    const int p = int(it - b * P);
+    const int c0 = p * CP;
+    int s = __ldg(states + b);
+    int tok = tokens ? __ldg(tokens + b) : 0;
+    __syncwarp();  // the previous item's reads of both buffers are done
+    fetch(s, 64, 0);  // count unknown: the whole blob
+    if (!triggered) {
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      triggered = true;
+    }
+    for (int k = 0; k < R; ++k) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      const int32_t *cur = reinterpret_cast<const int32_t *>(bufs + (k & 1) * S16);
+      const unsigned *wds = reinterpret_cast<const unsigned *>(cur + 4);
+      const uint16_t *rks = reinterpret_cast<const uint16_t *>(cur + 4 + Vw);
+      const int2 *ent = reinterpret_cast<const int2 *>(cur + E0);
+      const float acc = __int_as_float(cur[0]);
+      // successor from the blob, then the next blob's copy behind this step's stream
+      int sn = s, cn = 64;
+      int ntok = 0;
+      if (tokens) {
+        const unsigned tw = wds[tok >> 5];
+        const unsigned bp = unsigned(tok) & 31u;
+        if ((tw >> bp) & 1u) {
+          const int e = ent[int(rks[tok >> 5]) + __popc(tw & ((1u << bp) - 1u))].x;
+          sn = e & 0x1FFFFFF;
+          cn = int(unsigned(e) >> 25);
+        } else {
+          sn = s_next[tok];
+          cn = s_cnt[tok];
+        }
+      }
+      if (k + 1 < R) {
+        ntok = __ldg(tokens + int64_t(k + 1) * B + b);
+        fetch(sn, cn, (k + 1) & 1);
+      }
+      const int64_t rowoff = int64_t(k) * cells + b * V;
+      float4 *s4 = reinterpret_cast<float4 *>(scores + rowoff);
+      int4 *n4 = reinterpret_cast<int4 *>(next + rowoff);
+#pragma unroll 2
+      for (int c = c0 + lane; c < c0 + CP; c += 32) {
+        float4 r = r4[c];
+        int4 qv = q4[c];
+        r.x = acc + r.x;  // fp32 add, operand order as _kernels.pyx:70
+        r.y = acc + r.y;
+        r.z = acc + r.z;
+        r.w = acc + r.w;
+        const unsigned word = wds[c >> 3];
+        const int sh = (c & 7) * 4;
+        const unsigned bits = (word >> sh) & 0xFu;
+        if (bits) {
+          int q = int(rks[c >> 3]) + __popc(word & ((1u << sh) - 1u));
+          if (bits & 1u) { const int2 a = ent[q++]; r.x = __int_as_float(a.y); qv.x = a.x & 0x1FFFFFF; }
+          if (bits & 2u) { const int2 a = ent[q++]; r.y = __int_as_float(a.y); qv.y = a.x & 0x1FFFFFF; }
+          if (bits & 4u) { const int2 a = ent[q++]; r.z = __int_as_float(a.y); qv.z = a.x & 0x1FFFFFF; }
+          if (bits & 8u) { const int2 a = ent[q]; r.w = __int_as_float(a.y); qv.w = a.x & 0x1FFFFFF; }
+        }
+        adv_store(s4 + c, r);
+        adv_store(n4 + c, qv);
+      }
+      if (trace && p == 0 && lane == 0) trace[int64_t(k) * B + b] = s;
+      s = sn;
+      tok = ntok;
+      __syncwarp();  // this buffer is refilled two steps on
+    }
+    if (final_states && p == 0 && lane == 0) final_states[b] = s;
+  }
+  if (!triggered) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Successor gather for the generic chained path: s'[b] = next[b, tok[b]].
 __global__ void __launch_bounds__(256)
     gather_next_kernel(const int32_t *__restrict__ next, const int32_t *__restrict__ tok, int64_t B, int V,
@@ -740,12 +862,26 @@ static int launch_advance_steps(const pgpb_table *table, const int32_t *d_states
     // 89.0% vs 86.7% of the HBM peak at 8192 rows, 92.8% vs 89.1% at 65536,
     // equal at 1024 (profiles/r2_summary.md §4); the ranked-bitmap kernel
     // otherwise (tuning adv.compact = 1 forces it, for its tests)
-    auto fn = (t.adv_bits && tuning().adv_compact != 1) ? advance_steps_compact_kernel : advance_steps_kernel;
-    if (root_bytes > 48 * 1024)
+    // Kernel by regime (uniformly random states, profiles/r2_summary.md §4):
+    // up to R*B = 131072 rows per launch (<= 1 GiB of output) the launch is
+    // latency-bound and the advance blobs win (1024 rows x 32 steps: 87.6% vs
+    // 78.3% of the HBM peak, 8192 x 8: 91.9% vs 89.0%); above it the stream
+    // is bandwidth-bound and the compact arrays' smaller table footprint wins
+    // (8192 x 32: 93.1% vs 91.0%).  Tuning adv.compact: 1 ranked-bitmap
+    // kernel, 2 compact arrays, 3 blobs (tests).
+    const int lay = tuning().adv_compact;
+    auto fn = (t.adv_bits && lay != 1) ? advance_steps_compact_kernel : advance_steps_kernel;
+    size_t smem = root_bytes;
+    const bool blob = t.adv_blob && (lay == 3 || (lay == 0 && int64_t(R) * B <= 131072));
+    if (blob) {
+      fn = advance_steps_blob_kernel;
+      smem += size_t(kWarpsPerBlock) * 2 * size_t(t.adv_stride16) * 16 + size_t(t.vocab_padded);
+    }
+    if (smem > 48 * 1024)
       PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(root_bytes)));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     cudaLaunchAttribute attr[1];
-    cudaLaunchConfig_t cfg = pdl_config(dim3(unsigned(ctas)), dim3(kThreads), root_bytes, st, attr);
+    cudaLaunchConfig_t cfg = pdl_config(dim3(unsigned(ctas)), dim3(kThreads), smem, st, attr);
     PGPB_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, t, d_states, d_tokens, int(R), B, P, d_scores, d_next, d_trace,
                                      d_final));
     PGPB_CUDA_TRY(cudaGetLastError());

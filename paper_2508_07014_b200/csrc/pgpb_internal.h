@@ -20,7 +20,7 @@ struct Tuning {
   int ctc_segment = 0;    // frames per walker segment
   int ctc_seq = 0;        // 1 = sequential walk, 2 = speculative rounds only
   int ll_warps = 0;       // label-loop step: warps (rows) per CTA
-  int adv_compact = 0;    // chained advance: 0 compact table arrays when built, 1 the ranked-bitmap kernel
+  int adv_compact = 0;    // chained advance table layout: 0 by regime, 1 ranked bitmap, 2 compact arrays, 3 blobs
 };
 Tuning &tuning();
 
@@ -70,6 +70,15 @@ struct TableView {
   // halve the table bytes a uniformly random row pulls from HBM.
   const uint32_t *adv_bits;    // [S][Vw]
   const int2 *adv_clo;         // [C]
+  // Per-state advance blob, fixed stride (adv_stride16 x 16 B; NULL when
+  // V > 1024 or a closure does not fit): int32 [0] bits(acc_total),
+  // [1] closure count, [2..3] 0, [4, 4 + Vw) closure words, then Vw u16 word
+  // ranks, then the closure's {next | count(next) << 25, bits(score)} pairs
+  // (8-B aligned, at int32 index adv_ent0).  One warp-wide 16-B-per-lane copy
+  // of its used prefix brings a state's whole advance operand set.
+  const int4 *adv_blob;        // [S][adv_stride16]
+  int32_t adv_stride16;
+  int32_t adv_ent0;
 };
 
 }  // namespace pgpb

@@ -169,6 +169,31 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
     for (size_t i = 0; i < static_cast<size_t>(S) * Vw; ++i) adv_bits[i] = bits[2 * i];
   std::vector<int2> adv_clo(clo.size());
   for (size_t i = 0; i < clo.size(); ++i) adv_clo[i] = make_int2(clo[i].y, clo[i].z);
+  // fixed-stride advance blobs (pgpb_internal.h)
+  const int32_t ent0 = ((4 + Vw + (Vw + 1) / 2) + 1) & ~1;  // int32 index of the pairs, 8-B aligned
+  const int64_t blob_i32 = (int64_t(ent0) + 2 * int64_t(max_clo) + 31) / 32 * 32;  // 128-B multiple
+  // entries carry the successor's closure count in next's top bits (so a
+  // copy can be sized before the blob arrives): S < 2^25, counts < 2^6
+  const bool with_blob = with_adv && blob_i32 <= 256 && int64_t(S) * blob_i32 * 4 <= (int64_t(1) << 30) &&
+                         S < (1 << 25) && max_clo < 64;
+  std::vector<int32_t> adv_blob(with_blob ? static_cast<size_t>(S) * blob_i32 : 4, 0);
+  if (with_blob)
+    for (int32_t s0 = 0; s0 < S; ++s0) {
+      int32_t *w = adv_blob.data() + static_cast<size_t>(s0) * blob_i32;
+      const int4 r = clo_rec[s0];
+      w[0] = r.z;
+      w[1] = r.y;
+      uint16_t *rk = reinterpret_cast<uint16_t *>(w + 4 + Vw);
+      for (int32_t k = 0; k < Vw; ++k) {
+        w[4 + k] = static_cast<int32_t>(bits[2 * (static_cast<size_t>(s0) * Vw + k)]);
+        rk[k] = static_cast<uint16_t>(bits[2 * (static_cast<size_t>(s0) * Vw + k) + 1]);
+      }
+      for (int32_t i = 0; i < r.y; ++i) {
+        const int4 e = clo[static_cast<size_t>(r.x) + i];
+        w[ent0 + 2 * i] = e.y | (clo_rec[e.y].y << 25);
+        w[ent0 + 2 * i + 1] = e.z;
+      }
+    }
   std::vector<int32_t> rn_off(static_cast<size_t>(Vp), 0);
   for (int32_t v = 0; v < Vp; ++v) rn_off[v] = boff[root_next[v]];
 
@@ -192,6 +217,7 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   const int64_t o_bits = place(int64_t(bits.size()) * 4);
   const int64_t o_abits = place(int64_t(adv_bits.size()) * 4);
   const int64_t o_aclo = place(int64_t(adv_clo.size()) * 8);
+  const int64_t o_ablob = place(int64_t(adv_blob.size()) * 4);
   const int64_t total = off;
 
   int prev_dev = 0;
@@ -217,6 +243,7 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   std::memcpy(staging.data() + o_bits, bits.data(), bits.size() * 4);
   std::memcpy(staging.data() + o_abits, adv_bits.data(), adv_bits.size() * 4);
   std::memcpy(staging.data() + o_aclo, adv_clo.data(), adv_clo.size() * 8);
+  std::memcpy(staging.data() + o_ablob, adv_blob.data(), adv_blob.size() * 4);
   e = cudaMemcpy(arena, staging.data(), static_cast<size_t>(total), cudaMemcpyHostToDevice);
   cudaSetDevice(prev_dev);
   if (e != cudaSuccess) {
@@ -267,6 +294,9 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   v.bits_words = Vw;
   v.adv_bits = with_adv ? reinterpret_cast<const uint32_t *>(arena + o_abits) : nullptr;
   v.adv_clo = reinterpret_cast<const int2 *>(arena + o_aclo);
+  v.adv_blob = with_blob ? reinterpret_cast<const int4 *>(arena + o_ablob) : nullptr;
+  v.adv_stride16 = with_blob ? int32_t(blob_i32 / 4) : 0;
+  v.adv_ent0 = ent0;
   *out = t;
   return PGPB_OK;
 }

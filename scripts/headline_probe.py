@@ -18,9 +18,11 @@ tab, V = bw.table("p20k_v1024")
 dt = tab.device_table(0)
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+PARTS = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+LAYOUTS = [int(x) for x in sys.argv[4].split(",")] if len(sys.argv) > 4 else [0, 3]
 rng = np.random.default_rng(1000)
 big = B * R > 8192 * 8
-cases = [(n_in, 8 if big else 50, 2, cm) for cm in (1, 2) for n_in in ((8 if big else 50), 1)]
+cases = [(n_in, 8 if big else 50, 2, cm) for cm in LAYOUTS for n_in in ((8 if big else 50), 1)]
 for n_in, K, ring, cm in cases:
     _lib.set_tuning("adv.compact", cm)
     st = torch.from_numpy(rng.integers(0, tab.num_states, size=(n_in, B)).astype(np.int32)).cuda()
@@ -48,6 +50,6 @@ for n_in, K, ring, cm in cases:
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) / K)
     frac = [round(R * (B * V * 8 + B * 4) / (t / 1e3) / 1e9 / 6454.9, 3) for t in ts]
-    print(f"n_in={n_in} K={K} ring={ring} layout={cm} per-replay frac {frac}", flush=True)
+    print(f"B={B} R={R} P={PARTS} n_in={n_in} layout={cm} frac {frac}", flush=True)
     del outs, g
     torch.cuda.empty_cache()

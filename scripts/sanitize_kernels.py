@@ -30,8 +30,9 @@ toks = torch.from_numpy(rng.integers(0, V, size=(3, 300)).astype(np.int32)).to(d
 pb.advance_steps(tab, torch.from_numpy(st).to(dev), toks)  # compact arrays (V <= 1024)
 from paper_2508_07014_b200 import _lib  # noqa: E402
 
-_lib.set_tuning("adv.compact", 1)  # the ranked-bitmap chained kernel
-pb.advance_steps(tab, torch.from_numpy(st).to(dev), toks)
+for lay in (1, 2, 3):  # ranked-bitmap, compact-array and blob chained kernels
+    _lib.set_tuning("adv.compact", lay)
+    pb.advance_steps(tab, torch.from_numpy(st).to(dev), toks)
 _lib.set_tuning("adv.compact", 0)
 from paper_2508_07014_b200.table import _advance_device  # noqa: E402
 

@@ -103,7 +103,7 @@ def _closure_biased_tokens(tab, states0, R, rng, p_closure=0.6):
                                             ("p20k_v1024", 300, 5, 2), ("p20k_v1024", 97, 3, 8),
                                             ("p20k_v1024", 8192, 2, 0), ("p20k_v4096", 256, 3, 0),
                                             ("p5k_v1024", 4, 7, 0)])
-@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("layout", [0, 1, 2, 3])
 def test_advance_steps_vs_oracle(name, B, R, parts, layout):
     """Chained R-step advance (config 5): every step's rows bit-exact vs the
     oracle advance of that step's states, and s_{k+1} = next_k[b, tok_k[b]]."""
@@ -120,7 +120,7 @@ def test_advance_steps_vs_oracle(name, B, R, parts, layout):
     else:
         toks = rng.integers(0, V, size=(R, B)).astype(np.int32)
     from paper_2508_07014_b200 import _lib
-    _lib.set_tuning("adv.compact", layout)  # 0: compact arrays (V <= 1024), 1: the ranked-bitmap kernel
+    _lib.set_tuning("adv.compact", layout)  # 0 by regime, 1 ranked bitmap, 2 compact arrays, 3 blobs
     try:
         r = advance_steps(tab, torch.from_numpy(s0).cuda(), torch.from_numpy(toks).cuda(), parts=parts)
     finally:
@@ -282,11 +282,11 @@ def test_row_max_matches_oracle():
 
 
 @pytest.mark.parametrize("V,parts", [(896, 0), (512, 0), (512, 2), (256, 1), (128, 1)])
-@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("layout", [0, 1, 2, 3])
 def test_advance_steps_split_shapes(V, parts, layout):
     """Chained kernels at vocabularies below 1024 (compact arrays built, fewer
     than 32 bitmap words, one or two column parts; V = 896 leaves lanes 28-31
-    without a word), both table layouts, closure-biased token streams."""
+    without a word), every table layout, closure-biased token streams."""
     import torch
 
     from paper_2508_07014_b200 import _lib, advance_steps
