@@ -63,21 +63,28 @@ def test_advance_corpora_match_reference_golden(name):
     assert np.array_equal(c.next_states.cpu().numpy(), res.next_states)
 
 
-@pytest.mark.parametrize("chain", [False, True])
+@pytest.mark.parametrize("chain,single", [(False, 0), (False, 2), (True, 0)])
 @pytest.mark.parametrize("name,B", [("p20k_v1024", 8192), ("p20k_v4096", 2048), ("p5k_v1024", 3000),
                                     ("p20k_v1024", 37), ("p20k_v1024", 1024), ("p20k_v1024", 65)])
-def test_advance_full_size_vs_oracle(name, B, chain):
-    """The production advance (and the reference chain-walk kernel)
-    bit-exact against the oracle at the benchmark sizes."""
+def test_advance_full_size_vs_oracle(name, B, chain, single):
+    """The production advance (small batches through the blob kernel at one
+    step, the single-advance kernel otherwise or when forced by the tuning
+    key), and the reference chain-walk kernel, bit-exact against the oracle
+    at the benchmark sizes."""
     import torch
 
+    from paper_2508_07014_b200 import _lib
     from paper_2508_07014_b200.table import _advance_device
 
     phrases, V = gi.corpus(name)
     tab = product_table(phrases, V)
     rng = np.random.default_rng(B)
     states = rng.integers(0, tab.num_states, size=B).astype(np.int32)
-    d = _advance_device(tab, torch.from_numpy(states).cuda(), check=True, out=None, chain=chain)
+    _lib.set_tuning("adv.compact", single)
+    try:
+        d = _advance_device(tab, torch.from_numpy(states).cuda(), check=True, out=None, chain=chain)
+    finally:
+        _lib.set_tuning("adv.compact", 0)
     sc, nx = orc.score_batch(tab, states)
     assert bits_equal(d.scores.cpu().numpy(), sc)
     assert np.array_equal(d.next_states.cpu().numpy(), nx)
