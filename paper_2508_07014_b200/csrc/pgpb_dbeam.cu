@@ -293,6 +293,81 @@ __device__ __forceinline__ void mark_and_score_closures(const TableView &t, unsi
   worker_sync(t0);
 }
 
+// Advance blobs (TableView::adv_blob) of the expandable slots in shared
+// memory: one cp.async copy per slot brings the closure words (the dense
+// scan's exclusion bitmap), their ranks, the accumulator and the closure
+// pairs, replacing the record -> entries -> bitmap-marking round trips.
+__device__ __forceinline__ void db_cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
+// Copy the expandable slots' blobs, then publish {0, count, acc, 0} per slot
+// in s_rec (zero for slots that do not expand).  Worker threads [t0, ..).
+__device__ __forceinline__ void load_blobs(const TableView &t, int4 *blobs, const SBeam &s, const bool *expand,
+                                           int beam, int4 *s_rec, int t0) {
+  const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0, S16 = t.adv_stride16;
+  for (int i = tid; i < beam * S16; i += nt) {
+    const int h = i / S16;
+    if (expand[h]) db_cp_async16(blobs + i, t.adv_blob + int64_t(s.tree[h]) * S16 + (i - h * S16));
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  worker_sync(t0);
+  for (int h = tid; h < beam; h += nt) {
+    const int32_t *bl = reinterpret_cast<const int32_t *>(blobs + size_t(h) * S16);
+    s_rec[h] = expand[h] ? make_int4(0, bl[1], bl[0], 0) : make_int4(0, 0, 0, 0);
+  }
+  worker_sync(t0);
+}
+
+// Closure candidates of the expandable slots from their blobs: every set
+// bit of a slot's closure words is a first-hit arc, its pair the rank-th.
+template <int K>
+__device__ __forceinline__ void blob_closure_candidates(const TableView &t, const int4 *blobs, const SBeam &s,
+                                                        const bool *expand, int beam, const float *lp, int64_t ld,
+                                                        int64_t row0, int V, int skip, int special, double lam,
+                                                        Cand (&list)[K], int t0) {
+  const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
+  const int S16 = t.adv_stride16, Vw = t.bits_words, E0 = t.adv_ent0;
+  for (int i = tid; i < beam * Vw; i += nt) {
+    const int h = i / Vw, w = i - h * Vw;
+    if (!expand[h]) continue;
+    const int32_t *bl = reinterpret_cast<const int32_t *>(blobs + size_t(h) * S16);
+    unsigned word = static_cast<unsigned>(bl[4 + w]);
+    if (!word) continue;
+    int q = reinterpret_cast<const uint16_t *>(bl + 4 + Vw)[w];
+    const int2 *ent = reinterpret_cast<const int2 *>(bl + E0);
+    while (word) {
+      const int v = 32 * w + __ffs(word) - 1;
+      word &= word - 1;
+      const int2 e = ent[q++];
+      if (v == skip || v == special) continue;
+      const float x = lp[(row0 + h) * ld + v];
+      const double amv = __dadd_rn(s.am[h], static_cast<double>(x));
+      const double bv = __dadd_rn(s.boost[h], static_cast<double>(__int_as_float(e.y)));
+      list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + v});
+    }
+  }
+}
+
+// (score, next) of token v at a slot whose blob is in shared memory.
+__device__ __forceinline__ void blob_resolve(const TableView &t, const int4 *blob, const float *root, int v, float &sc,
+                                             int &nx) {
+  const int32_t *bl = reinterpret_cast<const int32_t *>(blob);
+  const int Vw = t.bits_words;
+  const unsigned w = static_cast<unsigned>(bl[4 + (v >> 5)]);
+  if ((w >> (v & 31)) & 1u) {
+    const int q = reinterpret_cast<const uint16_t *>(bl + 4 + Vw)[v >> 5] + __popc(w & ((1u << (v & 31)) - 1u));
+    const int2 e = reinterpret_cast<const int2 *>(bl + t.adv_ent0)[q];
+    sc = __int_as_float(e.y);
+    nx = e.x & 0x1FFFFFF;
+  } else {
+    sc = __int_as_float(bl[0]) + root[v];
+    nx = __ldg(t.root_next + v);
+  }
+}
+
 __device__ __forceinline__ void setup_root(const TableView &t, bool use_boost, int smem_root, unsigned char *smem,
                                            const float *&root, unsigned *&bm) {
   root = t.root_scores;
@@ -333,6 +408,7 @@ struct TBeamArgs {
   int J;
   const __nv_bfloat16 *pred_j;
   __nv_bfloat16 *z;
+  int blob_off;  // byte offset of the slots' advance blobs in dynamic shared memory (0: none)
 };
 
 __device__ __forceinline__ void write_hyp(const pgpb_beam_hyps &H, int64_t i, double am, double boost, int tree,
@@ -536,13 +612,23 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     Cand list[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+    int4 *blobs = (use_boost && a.blob_off) ? reinterpret_cast<int4 *>(smem + a.blob_off) : nullptr;
     if (int(threadIdx.x) >= t0) {
-      if (use_boost)
-        mark_and_score_closures<K>(tv, bm, bm_words, s, s_expand, beam, s_rec, LP, LD, R0, V, a.blank, -1, a.lam,
-                                   list, t0);
-      TB_MARK(2);
-      scan_candidates<K, kVec>(tv, root, bm, bm_words, LP, LD, R0, V, s, s_expand, beam, a.blank, -1, a.lam,
-                               use_boost, s_rec, list, t0, false);
+      if (blobs) {
+        load_blobs(tv, blobs, s, s_expand, beam, s_rec, t0);
+        blob_closure_candidates<K>(tv, blobs, s, s_expand, beam, LP, LD, R0, V, a.blank, -1, a.lam, list, t0);
+        TB_MARK(2);
+        // the blobs' closure words are the dense scan's exclusion bitmaps
+        scan_candidates<K, kVec>(tv, root, reinterpret_cast<const unsigned *>(blobs) + 4, tv.adv_stride16 * 4, LP,
+                                 LD, R0, V, s, s_expand, beam, a.blank, -1, a.lam, use_boost, s_rec, list, t0, false);
+      } else {
+        if (use_boost)
+          mark_and_score_closures<K>(tv, bm, bm_words, s, s_expand, beam, s_rec, LP, LD, R0, V, a.blank, -1, a.lam,
+                                     list, t0);
+        TB_MARK(2);
+        scan_candidates<K, kVec>(tv, root, bm, bm_words, LP, LD, R0, V, s, s_expand, beam, a.blank, -1, a.lam,
+                                 use_boost, s_rec, list, t0, false);
+      }
     }
     TB_MARK(3);
     block_topk<K>(list, beam, s_warp, s_win, s_key, s_am);
@@ -557,7 +643,10 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
       const int h = cid / V, v = cid % V;
       float sc = 0.0f;
       int nx = 0;
-      if (use_boost) resolve_ranked(tv, root, bm + h * ((V + 31) >> 5), s_rec[h], v, sc, nx);
+      if (blobs)
+        blob_resolve(tv, blobs + size_t(h) * tv.adv_stride16, root, v, sc, nx);
+      else if (use_boost)
+        resolve_ranked(tv, root, bm + h * ((V + 31) >> 5), s_rec[h], v, sc, nx);
       const int node = s_node_base + r;  // winners fill slots 0.. contiguously
       if (node >= S.trace.nmax) {
         *S.trace.overflow = 1;
@@ -778,9 +867,18 @@ static size_t beam_smem(const TableView &t, bool use_boost, int beam, int &smem_
 
 template <int K, typename Fn, typename Args>
 static int launch_beam(Fn fn, const Args &args, size_t smem, int64_t grid, cudaStream_t st) {
-  if (smem > 48 * 1024)
-    PGPB_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void *>(fn),
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  // static + dynamic shared memory above 48 KB needs the opt-in; the kernels'
+  // static part is ~27 KB, so opt in for any sizeable dynamic part (once per
+  // size for each kernel)
+  static thread_local size_t set_for[2] = {0, 0};
+  static thread_local const void *fn_for[2] = {nullptr, nullptr};
+  const void *f = reinterpret_cast<const void *>(fn);
+  const int slot = fn_for[0] == f ? 0 : (fn_for[1] == f ? 1 : (fn_for[0] ? 1 : 0));
+  if (smem > 16 * 1024 && (fn_for[slot] != f || set_for[slot] < smem)) {
+    PGPB_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    fn_for[slot] = f;
+    set_for[slot] = smem;
+  }
   fn<<<static_cast<unsigned>(grid), db_threads<K>(), smem, st>>>(args);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
@@ -831,7 +929,12 @@ int pgpb_tbeam_wave(const pgpb_table *table, const float *d_lp, int64_t ld, int6
   a.use_boost = use_boost ? 1 : 0;
   a.wave = wave;
   a.s = *state;
-  const size_t smem = beam_smem(a.t, use_boost, state->beam, a.smem_root);
+  size_t smem = beam_smem(a.t, use_boost, state->beam, a.smem_root);
+  if (use_boost && a.t.adv_blob && tuning().beam_blobs != 1) {
+    smem = (smem + 15) & ~size_t(15);
+    a.blob_off = int(smem);
+    smem += size_t(state->beam) * size_t(a.t.adv_stride16) * 16;
+  }
   const bool vec = (V % 4) == 0 && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(d_lp) % 16) == 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int k = state->beam;
@@ -882,8 +985,13 @@ int pgpb_tbeam_wave_fused(const pgpb_table *table, const void *d_logits_bf16, in
   beam_smem(a.t, use_boost, state->beam, smem_root);
   a.smem_root = smem_root;
   const size_t bm_bytes = size_t(state->beam) * size_t((V + 31) >> 5) * 4;
-  const size_t smem = (smem_root ? size_t(a.t.vocab_padded) * 4 : 0) + bm_bytes + 16 +
-                      size_t(state->beam) * size_t((V + 3) & ~3) * 4;
+  size_t smem = (smem_root ? size_t(a.t.vocab_padded) * 4 : 0) + bm_bytes + 16 +
+                size_t(state->beam) * size_t((V + 3) & ~3) * 4;
+  if (use_boost && a.t.adv_blob && tuning().beam_blobs != 1) {
+    smem = (smem + 15) & ~size_t(15);
+    a.blob_off = int(smem);
+    smem += size_t(state->beam) * size_t(a.t.adv_stride16) * 16;
+  }
   if (smem > 200 * 1024) return fail(PGPB_EINVAL, "beam x vocabulary too large for the fused wave");
   const bool vec = (V % 4) == 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

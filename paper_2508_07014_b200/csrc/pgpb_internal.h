@@ -20,6 +20,7 @@ struct Tuning {
   int ctc_segment = 0;    // frames per walker segment
   int ctc_seq = 0;        // 1 = sequential walk, 2 = speculative rounds only
   int ll_warps = 0;       // label-loop step: warps (rows) per CTA
+  int beam_blobs = 0;     // device beams: 0 advance blobs when built, 1 closure records + bitmap marking
   int adv_compact = 0;    // chained advance table layout: 0 by regime, 1 ranked bitmap, 2 compact arrays, 3 blobs
 };
 Tuning &tuning();
