@@ -70,8 +70,17 @@ def _tbeam_case(lam, beam, cap, rollback=False, use_graph=False, B=5, T=9, V=48,
 
 
 @pytest.mark.parametrize("lam,beam,cap", [(1.0, 4, 2), (2.0, 3, 3), (0.0, 4, 2), (1.5, 8, 1), (1.0, 1, 2)])
-def test_transducer_device_beam_matches_reference_by_replay(lam, beam, cap):
-    _tbeam_case(lam, beam, cap)
+@pytest.mark.parametrize("blobs", [0, 1])
+def test_transducer_device_beam_matches_reference_by_replay(lam, beam, cap, blobs):
+    """blobs = 0: closure data from the table's advance blobs (V <= 1024),
+    1: closure records + bitmap marking (the path for larger vocabularies)."""
+    from paper_2508_07014_b200 import _lib
+
+    _lib.set_tuning("beam.blobs", blobs)
+    try:
+        _tbeam_case(lam, beam, cap)
+    finally:
+        _lib.set_tuning("beam.blobs", 0)
 
 
 def test_transducer_device_beam_rollback():
