@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   unsigned char *s_cnt = reinterpret_cast<unsigned char *>(smem + size_t(Vp) * 8 + size_t(blockDim.x >> 5) * 2 * S16 * 16);
   stage_root(t, s_root, s_next);
   __syncthreads();
-  for (int v = threadIdx.x; v < V; v += blockDim.x) s_cnt[v] = static_cast<unsigned char>(__ldg(&t.clo_rec[s_next[v]].y));
+  for (int v = threadIdx.x; v < V; v += blockDim.x) s_cnt[v] = __ldg(t.adv_root_cnt + v);
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int W = blockDim.x >> 5;

@@ -78,6 +78,7 @@ struct TableView {
   // (8-B aligned, at int32 index adv_ent0).  One warp-wide 16-B-per-lane copy
   // of its used prefix brings a state's whole advance operand set.
   const int4 *adv_blob;        // [S][adv_stride16]
+  const uint8_t *adv_root_cnt; // [Vp] closure count of root_next[v] (sizes a dense successor's blob copy)
   int32_t adv_stride16;
   int32_t adv_ent0;
 };

@@ -194,6 +194,9 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
         w[ent0 + 2 * i + 1] = e.z;
       }
     }
+  std::vector<uint8_t> root_cnt(static_cast<size_t>(Vp), 0);
+  if (with_blob)
+    for (int32_t v = 0; v < V; ++v) root_cnt[v] = static_cast<uint8_t>(clo_rec[root_next[v]].y);
   std::vector<int32_t> rn_off(static_cast<size_t>(Vp), 0);
   for (int32_t v = 0; v < Vp; ++v) rn_off[v] = boff[root_next[v]];
 
@@ -218,6 +221,7 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   const int64_t o_abits = place(int64_t(adv_bits.size()) * 4);
   const int64_t o_aclo = place(int64_t(adv_clo.size()) * 8);
   const int64_t o_ablob = place(int64_t(adv_blob.size()) * 4);
+  const int64_t o_rcnt = place(int64_t(Vp));
   const int64_t total = off;
 
   int prev_dev = 0;
@@ -244,6 +248,7 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   std::memcpy(staging.data() + o_abits, adv_bits.data(), adv_bits.size() * 4);
   std::memcpy(staging.data() + o_aclo, adv_clo.data(), adv_clo.size() * 8);
   std::memcpy(staging.data() + o_ablob, adv_blob.data(), adv_blob.size() * 4);
+  std::memcpy(staging.data() + o_rcnt, root_cnt.data(), size_t(Vp));
   e = cudaMemcpy(arena, staging.data(), static_cast<size_t>(total), cudaMemcpyHostToDevice);
   cudaSetDevice(prev_dev);
   if (e != cudaSuccess) {
@@ -296,6 +301,7 @@ static int pgpb_table_create_impl(int32_t S, int32_t V, int32_t A, const int32_t
   v.adv_clo = reinterpret_cast<const int2 *>(arena + o_aclo);
   v.adv_blob = with_blob ? reinterpret_cast<const int4 *>(arena + o_ablob) : nullptr;
   v.adv_stride16 = with_blob ? int32_t(blob_i32 / 4) : 0;
+  v.adv_root_cnt = reinterpret_cast<const uint8_t *>(arena + o_rcnt);
   v.adv_ent0 = ent0;
   *out = t;
   return PGPB_OK;
