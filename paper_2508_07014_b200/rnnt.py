@@ -286,9 +286,12 @@ class LabelLoopingDecoder:
         with torch.cuda.stream(s):  # warm-up allocations outside the capture
             self._iteration()
         torch.cuda.current_stream(self.dev).wait_stream(s)
+        # one poll interval of iterations per graph: one launch per host check
+        # (iterations past the end are no-ops on finished rows)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self._iteration()
+            for _ in range(self.poll):
+                self._iteration()
         self.graph = g
 
     def decode(self, enc_proj, lengths=None, *, record: bool = False, max_iters: int | None = None) -> LabelLoopOutput:
@@ -302,7 +305,10 @@ class LabelLoopingDecoder:
         it = 0
         while it < limit:
             steps = min(self.poll, limit - it)
-            for _ in range(steps):
+            graphed = self.graph is not None and not record and steps == self.poll
+            if graphed:
+                self.graph.replay()  # self.poll iterations
+            for _ in range(0 if graphed else steps):
                 if record:
                     t0, last0 = self.t.clone(), self.last.clone()
                     active = (t0 < self.lengths).cpu().numpy()
@@ -311,8 +317,6 @@ class LabelLoopingDecoder:
                     if self.dur is not None:
                         rec = rec + (self.dur.cpu().numpy().copy(),)
                     records.append(rec)
-                elif self.graph is not None:
-                    self.graph.replay()
                 else:
                     self._iteration()
             it += steps
