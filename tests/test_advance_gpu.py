@@ -315,3 +315,32 @@ def test_advance_steps_split_shapes(V, parts, layout):
         assert bits_equal(r.scores[k].cpu().numpy(), sc) and np.array_equal(r.next_states[k].cpu().numpy(), nx)
         s = nx[np.arange(B), toks[k]].astype(np.int32)
     assert np.array_equal(r.final_states.cpu().numpy(), s)
+
+
+def test_advance_without_blobs_falls_back():
+    """A state whose closure has >= 64 first-hit arcs (a root child with 100
+    children) leaves the advance blobs unbuilt: single and chained advances
+    then run on the compact arrays and stay bit-exact."""
+    import torch
+
+    from paper_2508_07014_b200 import advance_steps
+
+    V = 256
+    phrases = [(1, v) for v in range(2, 102)] + [(3, 4, 5), (7, 8)]
+    tab = product_table(phrases, V)
+    assert tab.device_table().info().max_closure >= 64
+    rng = np.random.default_rng(64)
+    B, R = 300, 4
+    s0 = rng.integers(0, tab.num_states, size=B).astype(np.int32)
+    toks = _closure_biased_tokens(tab, s0, R, rng)
+    r = advance_steps(tab, torch.from_numpy(s0).cuda(), torch.from_numpy(toks).cuda())
+    s = s0
+    for k in range(R):
+        sc, nx = orc.score_batch(tab, s)
+        assert bits_equal(r.scores[k].cpu().numpy(), sc) and np.array_equal(r.next_states[k].cpu().numpy(), nx)
+        s = nx[np.arange(B), toks[k]].astype(np.int32)
+    from paper_2508_07014_b200.table import _advance_device
+
+    d = _advance_device(tab, torch.from_numpy(s0).cuda(), check=True, out=None)
+    sc, nx = orc.score_batch(tab, s0)
+    assert bits_equal(d.scores.cpu().numpy(), sc) and np.array_equal(d.next_states.cpu().numpy(), nx)
