@@ -299,9 +299,6 @@ int pgpb_rnnt_joint_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, cons
 int pgpb_rnnt_beam_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, const int32_t *d_t,
                           const int32_t *d_lengths, const void *d_pred_j, const int32_t *d_last, int64_t B,
                           int32_t K, int32_t blank, void *d_z, void *stream);
-/* Row log-softmax of bf16 logits into fp32 (torch's formula order).     */
-int pgpb_log_softmax_bf16(const void *d_x, int64_t ldx, float *d_y, int64_t ldy, int64_t rows, int32_t V,
-                          void *stream);
 int pgpb_rnnt_lstm_update(const void *d_E, const int64_t *d_feed, const void *d_hg, int64_t ld_hg,
                           const uint8_t *d_emit, void *d_h, void *d_c, int64_t B, int32_t H, void *stream);
 

@@ -130,7 +130,6 @@ _SIGS = {
                                     POINTER(LabelLoopState), _P, _P, _P, c_void_p],
     "pgpb_rnnt_joint_hidden": [_P, c_int64, c_int32, _P, _P, _P, c_int64, _P, c_int64, c_void_p],
     "pgpb_rnnt_beam_hidden": [_P, c_int64, c_int32, _P, _P, _P, _P, c_int64, c_int32, c_int32, _P, c_void_p],
-    "pgpb_log_softmax_bf16": [_P, c_int64, _P, c_int64, c_int64, c_int32, c_void_p],
     "pgpb_rnnt_lstm_update": [_P, _P, _P, c_int64, _P, _P, _P, c_int64, c_int32, c_void_p],
     "pgpb_beam_topk": [c_void_p, _P, c_int64, c_int64, c_int32, c_int32, c_int32, _P, _P, _P, _P,
                        _P, _P, _P, c_double, c_int32, c_int32, _P, _P, _P, _P, _P, _P, c_void_p],

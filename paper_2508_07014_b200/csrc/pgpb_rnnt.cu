@@ -126,27 +126,6 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Row log-softmax, bf16 in, fp32 out (torch's formula order), one warp per row.
-__global__ void __launch_bounds__(256)
-    log_softmax_bf16_kernel(const __nv_bfloat16 *__restrict__ x, int64_t ldx, float *__restrict__ y, int64_t ldy,
-                            int64_t R, int V) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (r >= R) return;
-  const __nv_bfloat16 *xr = x + r * ldx;
-  float *yr = y + r * ldy;
-  float m = -INFINITY;
-  for (int v = lane; v < V; v += 32) m = fmaxf(m, __bfloat162float(xr[v]));
-  float mr;
-  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(m));
-  float s = 0.0f;
-  for (int v = lane; v < V; v += 32) s += expf(__bfloat162float(xr[v]) - mr);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  const float ls = logf(s);
-  for (int v = lane; v < V; v += 32) yr[v] = (__bfloat162float(xr[v]) - mr) - ls;
-}
-
 }  // namespace pgpb
 
 extern "C" {
@@ -164,19 +143,6 @@ int pgpb_rnnt_beam_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, const
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;
 }
-
-int pgpb_log_softmax_bf16(const void *d_x, int64_t ldx, float *d_y, int64_t ldy, int64_t R, int32_t V,
-                          void *stream) {
-  using namespace pgpb;
-  if (R < 0 || V < 1 || ldx < V || ldy < V) return fail(PGPB_EINVAL, "bad shape");
-  if (R == 0) return PGPB_OK;
-  if (!d_x || !d_y) return fail(PGPB_EINVAL, "NULL buffer");
-  log_softmax_bf16_kernel<<<unsigned((R + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16 *>(d_x), ldx, d_y, ldy, R, V);
-  PGPB_CUDA_TRY(cudaGetLastError());
-  return PGPB_OK;
-}
-
 
 int pgpb_rnnt_joint_hidden(const void *d_enc_proj, int64_t ld_b, int32_t J, const int64_t *d_t,
                            const int64_t *d_lengths, const void *d_pred_proj, int64_t ld_pred, void *d_z, int64_t B,

@@ -1,6 +1,7 @@
 """Bench-shape workloads for one-kernel ncu captures (scripts/gpu_ncu_kernels.sh).
 
-python scripts/ncu_workloads.py {config3|config4|aed_greedy|beam_api|hits|ctc_ref}
+python scripts/ncu_workloads.py {config3|config3_unfused|config4|aed_greedy|beam_api|hits|label_loop|greedy_host|
+                                 advance_single|table_helpers|ctc_clean_boosted|ctc_clean_unboosted}
 """
 import sys
 from pathlib import Path
@@ -59,6 +60,29 @@ elif what == "label_loop":
     model, tab, enc_proj = bw.config2(dev)
     c = bw.C2
     LabelLoopingDecoder(model, tab, pb.DecodeConfig(lam=1.0), c["B"], c["T"], use_graph=False).decode(enc_proj)
+elif what == "greedy_host":  # transducer_greedy_boosted with a host StepModel (pgpb_greedy_step)
+    tab, V = bw.table("p5k_v1024")
+    rng = np.random.default_rng(5)
+    rows, default = gi.random_transducer_rows(rng, V)
+    m = pb.TableStepModel(flavor="transducer", default_row=default, rows=rows)
+    pb.transducer_greedy_boosted(m, 30, 0, tab, pb.DecodeConfig(lam=1.0))
+elif what == "advance_single":  # get_scores_batch on device tensors, 8192 rows (advance_v6_kernel)
+    tab, V = bw.table("p20k_v1024")
+    st = torch.from_numpy(np.random.default_rng(1).integers(0, tab.num_states, size=8192).astype(np.int32)).to(dev)
+    for _ in range(4):
+        pb.get_scores_batch(tab, st)
+elif what == "table_helpers":  # per-table precomputations (row_max, final_bonus, backoff_total)
+    tab, V = bw.table("p20k_v1024")
+    dt = tab.device_table(0)
+    dt.row_max(), dt.final_bonus(), dt.backoff_total()
+elif what == "config3_unfused":  # beam_hidden_kernel + log_softmax_bf16_kernel (the unfused wave)
+    from paper_2508_07014_b200.beams import TransducerBeamDecoder
+
+    model, tab, enc = bw.config3(dev)
+    c = bw.C3
+    dec = TransducerBeamDecoder(model, tab, pb.DecodeConfig(lam=1.0, beam_size=4, max_symbols_per_frame=5), c["B"],
+                                c["T"], use_graph=False, fused=False)
+    dec.run(enc, torch.full((c["B"],), 4))
 torch.cuda.synchronize()
 print("ok", what)
 if what.startswith("ctc_clean"):
