@@ -168,12 +168,7 @@ __global__ void __launch_bounds__(kBeamThreads) beam_topk_kernel(BeamArgs a) {
 
     // Block merge: `rounds` rounds of argmax over the per-thread list heads.
     for (int r = 0; r < rounds; ++r) {
-      Cand best = list[0];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const Cand oc = shfl_cand(best, o);
-        if (cand_better(oc, best)) best = oc;
-      }
+      const Cand best = cand_warp_best(list[0]);
       if (lane == 0) s_warp[wid] = best;
       __syncthreads();
       if (threadIdx.x == 0) {

@@ -49,6 +49,45 @@ __device__ __forceinline__ Cand shfl_cand(const Cand &c, int o) {
   return r;
 }
 
+// Order-preserving unsigned key of a double (NaN excluded), -0.0 folded onto
+// +0.0 so equal values compare equal as in cand_better.
+__device__ __forceinline__ unsigned long long cand_dkey(double x) {
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(x, 0.0)));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// Warp argmax in cand_better's order with hardware reductions: the 64-bit
+// key's two halves by redux.sync, am and then cid only among exact key ties,
+// the winner shuffled from its lane (three shuffles instead of five
+// butterfly levels of compares and fifteen shuffles).  Every lane returns it.
+__device__ __forceinline__ Cand cand_warp_best(const Cand &mine) {
+  const bool has = mine.cid != INT_MAX;
+  const unsigned long long k = has ? cand_dkey(mine.key) : 0ull;
+  const unsigned hi = unsigned(k >> 32), lo = unsigned(k);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  unsigned tie = __ballot_sync(0xffffffffu, has && hi == mhi && lo == mlo);
+  if (__popc(tie) > 1) {
+    const bool in = (tie >> (threadIdx.x & 31)) & 1u;
+    const unsigned long long a = in ? cand_dkey(mine.am) : 0ull;
+    const unsigned ahi = unsigned(a >> 32), alo = unsigned(a);
+    const unsigned mahi = __reduce_max_sync(0xffffffffu, ahi);
+    const unsigned malo = __reduce_max_sync(0xffffffffu, ahi == mahi ? alo : 0u);
+    tie = __ballot_sync(0xffffffffu, in && ahi == mahi && alo == malo);
+    if (__popc(tie) > 1) {
+      const bool in2 = (tie >> (threadIdx.x & 31)) & 1u;
+      const unsigned mc = __reduce_min_sync(0xffffffffu, in2 ? unsigned(mine.cid) : 0xffffffffu);
+      tie = __ballot_sync(0xffffffffu, in2 && unsigned(mine.cid) == mc);
+    }
+  }
+  const int src = tie ? __ffs(tie) - 1 : 0;
+  Cand w;
+  w.key = __shfl_sync(0xffffffffu, mine.key, src);
+  w.am = __shfl_sync(0xffffffffu, mine.am, src);
+  w.cid = __shfl_sync(0xffffffffu, mine.cid, src);
+  return w;
+}
+
 // Resolve (score, next) of token v at a state via closure binary search.
 __device__ __forceinline__ void resolve_cell(const TableView &t, const float *root, const int32_t *rnext,
                                              int state, int v, float &s, int &nx) {

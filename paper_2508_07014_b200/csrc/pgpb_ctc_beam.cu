@@ -290,12 +290,7 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
       // 4. top `beam` in two levels: each warp pops its own top from its
       // lanes' lists (shuffles only), then warp 0 merges the warps' lists
       for (int r = 0; r < beam; ++r) {
-        Cand best = list[0];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const Cand oc = shfl_cand(best, o);
-          if (cand_better(oc, best)) best = oc;
-        }
+        const Cand best = cand_warp_best(list[0]);
         if (lane == 0) s_wl[wid * beam + r] = best;
         if (best.cid != INT_MAX && list[0].cid == best.cid) list_pop<K>(list);
       }
@@ -307,12 +302,7 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
         const int nw = blockDim.x >> 5;
         for (int j = lane; j < nw * beam; j += 32) list_insert<K>(l2, s_wl[j]);
         for (int r = 0; r < beam; ++r) {
-          Cand best = l2[0];
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            const Cand oc = shfl_cand(best, o);
-            if (cand_better(oc, best)) best = oc;
-          }
+          const Cand best = cand_warp_best(l2[0]);
           if (lane == 0) {
             s_win[r] = best.cid;
             s_key[r] = best.key;

@@ -195,12 +195,7 @@ __device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp,
   __shared__ Cand s_wl[kDbMaxWarps * kMaxTopK];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = 0; r < k; ++r) {
-    Cand best = list[0];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const Cand oc = shfl_cand(best, o);
-      if (cand_better(oc, best)) best = oc;
-    }
+    const Cand best = cand_warp_best(list[0]);
     if (lane == 0) s_wl[wid * k + r] = best;
     if (best.cid != INT_MAX && list[0].cid == best.cid) list_pop<K>(list);
   }
@@ -211,12 +206,7 @@ __device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp,
     for (int i = 0; i < K; ++i) l2[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
     for (int j = lane; j < nw * k; j += 32) list_insert<K>(l2, s_wl[j]);
     for (int r = 0; r < k; ++r) {
-      Cand best = l2[0];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const Cand oc = shfl_cand(best, o);
-        if (cand_better(oc, best)) best = oc;
-      }
+      const Cand best = cand_warp_best(l2[0]);
       if (lane == 0) {
         s_win[r] = best.cid;
         s_key[r] = best.key;
