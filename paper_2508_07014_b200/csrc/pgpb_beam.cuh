@@ -88,6 +88,29 @@ __device__ __forceinline__ Cand cand_warp_best(const Cand &mine) {
   return w;
 }
 
+// Warp-level merge of nw <= 32 per-warp top-k lists s_wl[w * k + i] (each
+// sorted best first, empty entries cid == INT_MAX) into the block's top k:
+// lane w holds warp w's current head, each round takes the warp best and the
+// winning lane advances — no re-insertion of the nw * k entries.
+__device__ __forceinline__ void merge_warp_lists(const Cand *s_wl, int nw, int k, int lane, int *s_win,
+                                                 double *s_key, double *s_am) {
+  const Cand none{-INFINITY, -INFINITY, INT_MAX};
+  int ptr = 0;
+  Cand head = lane < nw ? s_wl[lane * k] : none;
+  for (int r = 0; r < k; ++r) {
+    const Cand best = cand_warp_best(head);
+    if (lane == 0) {
+      s_win[r] = best.cid;
+      s_key[r] = best.key;
+      s_am[r] = best.am;
+    }
+    if (best.cid != INT_MAX && head.cid == best.cid) {
+      ++ptr;
+      head = ptr < k ? s_wl[lane * k + ptr] : none;
+    }
+  }
+}
+
 // Resolve (score, next) of token v at a state via closure binary search.
 __device__ __forceinline__ void resolve_cell(const TableView &t, const float *root, const int32_t *rnext,
                                              int state, int v, float &s, int &nx) {

@@ -295,22 +295,7 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
         if (best.cid != INT_MAX && list[0].cid == best.cid) list_pop<K>(list);
       }
       __syncthreads();
-      if (wid == 0) {
-        Cand l2[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) l2[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
-        const int nw = blockDim.x >> 5;
-        for (int j = lane; j < nw * beam; j += 32) list_insert<K>(l2, s_wl[j]);
-        for (int r = 0; r < beam; ++r) {
-          const Cand best = cand_warp_best(l2[0]);
-          if (lane == 0) {
-            s_win[r] = best.cid;
-            s_key[r] = best.key;
-            s_am[r] = best.am;
-          }
-          if (best.cid != INT_MAX && l2[0].cid == best.cid) list_pop<K>(l2);
-        }
-      }
+      if (wid == 0) merge_warp_lists(s_wl, int(blockDim.x >> 5), beam, lane, s_win, s_key, s_am);
       __syncthreads();
       // 5. the next beam
       if (threadIdx.x < beam) {

@@ -186,7 +186,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
 }
 
 // Block top-k in two levels: each warp pops its own top k from its lanes'
-// lists with warp shuffles only, then warp 0 merges the warps' k-lists —
+// lists with warp reductions, then warp 0 merges the warps' sorted k-lists head by head —
 // two block barriers in total instead of two per round.
 template <int K>
 __device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp, int *s_win, double *s_key,
@@ -200,21 +200,7 @@ __device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp,
     if (best.cid != INT_MAX && list[0].cid == best.cid) list_pop<K>(list);
   }
   __syncthreads();
-  if (wid == 0) {
-    Cand l2[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) l2[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
-    for (int j = lane; j < nw * k; j += 32) list_insert<K>(l2, s_wl[j]);
-    for (int r = 0; r < k; ++r) {
-      const Cand best = cand_warp_best(l2[0]);
-      if (lane == 0) {
-        s_win[r] = best.cid;
-        s_key[r] = best.key;
-        s_am[r] = best.am;
-      }
-      if (best.cid != INT_MAX && l2[0].cid == best.cid) list_pop<K>(l2);
-    }
-  }
+  if (wid == 0) merge_warp_lists(s_wl, nw, k, lane, s_win, s_key, s_am);
   __syncthreads();
 }
 
