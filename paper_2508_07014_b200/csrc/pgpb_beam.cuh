@@ -111,6 +111,123 @@ __device__ __forceinline__ void merge_warp_lists(const Cand *s_wl, int nw, int k
   }
 }
 
+// Candidate whose ranking key is pre-folded to its order-preserving integer
+// image (cand_dkey; 0 = empty): the per-thread list insertions and the warp
+// reductions compare 64-bit integers, predicated, instead of chains of fp64
+// compares whose per-lane outcomes diverge the warp; am and then cid only
+// break exact key ties, so the order is cand_better's.
+struct KCand {
+  unsigned long long k;
+  double am;
+  int cid;
+};
+
+__device__ __forceinline__ KCand kcand(double key, double am, int cid) { return KCand{cand_dkey(key), am, cid}; }
+__device__ __forceinline__ KCand kcand_none() { return KCand{0ull, -INFINITY, INT_MAX}; }
+
+// Inverse of cand_dkey (-0.0 comes back as +0.0).
+__device__ __forceinline__ double kcand_key(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double(static_cast<long long>(u));
+}
+
+__device__ __forceinline__ bool kc_better(const KCand &a, const KCand &b) {
+  if (a.k != b.k) return a.k > b.k;
+  if (a.am != b.am) return a.am > b.am;
+  return a.cid < b.cid;
+}
+
+template <int K>
+__device__ __forceinline__ void klist_insert(KCand (&l)[K], const KCand &c) {
+  if (!kc_better(c, l[K - 1])) return;
+  l[K - 1] = c;
+#pragma unroll
+  for (int i = K - 1; i > 0; --i) {
+    const bool sw = kc_better(l[i], l[i - 1]);
+    const KCand x = l[i], y = l[i - 1];
+    l[i - 1].k = sw ? x.k : y.k;
+    l[i - 1].am = sw ? x.am : y.am;
+    l[i - 1].cid = sw ? x.cid : y.cid;
+    l[i].k = sw ? y.k : x.k;
+    l[i].am = sw ? y.am : x.am;
+    l[i].cid = sw ? y.cid : x.cid;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void klist_pop(KCand (&l)[K]) {
+#pragma unroll
+  for (int i = 0; i < K - 1; ++i) l[i] = l[i + 1];
+  l[K - 1] = kcand_none();
+}
+
+// cand_warp_best on pre-folded keys.
+__device__ __forceinline__ KCand kc_warp_best(const KCand &mine) {
+  const bool has = mine.cid != INT_MAX;
+  const unsigned long long k = has ? mine.k : 0ull;
+  const unsigned hi = unsigned(k >> 32), lo = unsigned(k);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  unsigned tie = __ballot_sync(0xffffffffu, has && hi == mhi && lo == mlo);
+  if (__popc(tie) > 1) {
+    const bool in = (tie >> (threadIdx.x & 31)) & 1u;
+    const unsigned long long a = in ? cand_dkey(mine.am) : 0ull;
+    const unsigned ahi = unsigned(a >> 32), alo = unsigned(a);
+    const unsigned mahi = __reduce_max_sync(0xffffffffu, ahi);
+    const unsigned malo = __reduce_max_sync(0xffffffffu, ahi == mahi ? alo : 0u);
+    tie = __ballot_sync(0xffffffffu, in && ahi == mahi && alo == malo);
+    if (__popc(tie) > 1) {
+      const bool in2 = (tie >> (threadIdx.x & 31)) & 1u;
+      const unsigned mc = __reduce_min_sync(0xffffffffu, in2 ? unsigned(mine.cid) : 0xffffffffu);
+      tie = __ballot_sync(0xffffffffu, in2 && unsigned(mine.cid) == mc);
+    }
+  }
+  const int src = tie ? __ffs(tie) - 1 : 0;
+  KCand w;
+  w.k = __shfl_sync(0xffffffffu, mine.k, src);
+  w.am = __shfl_sync(0xffffffffu, mine.am, src);
+  w.cid = __shfl_sync(0xffffffffu, mine.cid, src);
+  return w;
+}
+
+// merge_warp_lists on pre-folded keys.
+__device__ __forceinline__ void kmerge_warp_lists(const KCand *s_wl, int nw, int k, int lane, int *s_win,
+                                                  double *s_key, double *s_am) {
+  int ptr = 0;
+  KCand head = lane < nw ? s_wl[lane * k] : kcand_none();
+  for (int r = 0; r < k; ++r) {
+    const KCand best = kc_warp_best(head);
+    if (lane == 0) {
+      s_win[r] = best.cid;
+      s_key[r] = best.cid != INT_MAX ? kcand_key(best.k) : -INFINITY;
+      s_am[r] = best.am;
+    }
+    if (best.cid != INT_MAX && head.cid == best.cid) {
+      ++ptr;
+      head = ptr < k ? s_wl[lane * k + ptr] : kcand_none();
+    }
+  }
+}
+
+// Order-preserving u32 image of a float (NaN excluded) and its inverse.
+__device__ __forceinline__ unsigned ford(float x) {
+  const unsigned u = __float_as_uint(x);
+  return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ford_inv(unsigned k) { return __uint_as_float((k >> 31) ? (k & 0x7FFFFFFFu) : ~k); }
+
+// k-th largest (1-based, counted with multiplicity) of the lanes' x, k <= 32;
+// -inf when fewer than k lanes remain.  All 32 lanes must call it.
+__device__ __forceinline__ float warp_kth_max(float x, int k) {
+  unsigned u = ford(x), m = 0u;
+  for (int r = 0; r < k; ++r) {
+    m = __reduce_max_sync(0xffffffffu, u);
+    const unsigned b = __ballot_sync(0xffffffffu, u == m);
+    if (int(threadIdx.x & 31) == __ffs(b) - 1) u = 0u;
+  }
+  return m ? ford_inv(m) : -INFINITY;
+}
+
 // Resolve (score, next) of token v at a state via closure binary search.
 __device__ __forceinline__ void resolve_cell(const TableView &t, const float *root, const int32_t *rnext,
                                              int state, int v, float &s, int &nx) {

@@ -68,10 +68,15 @@ __device__ bool cb_same_tokens(const int32_t *parent, const int32_t *token, int 
   return true;
 }
 
+// One beam.  tot = logaddexp(pb, pnb), known when the slot is filled (the
+// winner's am: a carried prefix's am is that very logaddexp, a new prefix
+// has pb = -inf), so no frame recomputes it; pnode = the trace node the
+// prefix's last token was appended to (its parent's node), so the parent
+// search confirms the usual case without reading the trace.
 struct Slots {
-  double pb[kMaxTopK], pnb[kMaxTopK], boost[kMaxTopK];
+  double pb[kMaxTopK], pnb[kMaxTopK], tot[kMaxTopK], boost[kMaxTopK];
   uint64_t hash[kMaxTopK], phash[kMaxTopK];
-  int tree[kMaxTopK], last[kMaxTopK], node[kMaxTopK], len[kMaxTopK];
+  int tree[kMaxTopK], last[kMaxTopK], node[kMaxTopK], pnode[kMaxTopK], len[kMaxTopK];
 };
 
 struct CbArgs {
@@ -101,20 +106,41 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
                : "memory");
 }
 
+#ifdef PGPB_CB_PROFILE
+// Debug-only CTA-0 phase timeline (pgpb_debug_cb_profile): [i] cycles spent
+// in phase i summed over frames (thread 0, measured after each barrier),
+// [15] frames.
+__device__ unsigned long long g_cb_prof[16];
+#define CB_MARK(i)                                                      \
+  do {                                                                  \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                          \
+      const long long n_ = clock64();                                   \
+      g_cb_prof[i] += (unsigned long long)(n_ - t_mark);                \
+      t_mark = n_;                                                      \
+    }                                                                   \
+  } while (0)
+#else
+#define CB_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 template <int K, bool kVec>
 __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
+#ifdef PGPB_CB_PROFILE
+  long long t_mark = clock64();
+#endif
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ Slots cur, nxt;
-  __shared__ int s_par[kMaxTopK], s_n;
-  __shared__ double s_cpb[kMaxTopK], s_cpnb[kMaxTopK], s_tot[kMaxTopK];
+  __shared__ Slots sl[2];  // this frame's beam and the next (swapped by frame parity)
+  __shared__ int s_par[kMaxTopK];
+  __shared__ double s_cpb[kMaxTopK], s_cpnb[kMaxTopK], s_amj[kMaxTopK];
   // closure records of the live prefixes' states, double-buffered: the next
   // frame's are fetched (cp.async, own commit group) as soon as the winners'
   // states are known, and waited for only after the next frame's carries
   __shared__ __align__(16) int4 s_rec2[2][kMaxTopK];
-  __shared__ Cand s_wl[kCbMaxWarps * kMaxTopK];
+  __shared__ KCand s_wl[kCbMaxWarps * kMaxTopK];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
-  __shared__ int s_nodes;
   const TableView &t = a.t;
   const int V = a.V, Vp = (V + 3) & ~3, Vw = (V + 31) >> 5, beam = a.beam;
   const bool boost = a.use_boost != 0;
@@ -137,18 +163,21 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
     int32_t *np = a.tr_parent + nb, *nt = a.tr_token + nb;
     __syncthreads();
     if (threadIdx.x == 0) {
-      cur.pb[0] = 0.0;
-      cur.pnb[0] = -INFINITY;
-      cur.boost[0] = 0.0;
-      cur.hash[0] = 0ull;
-      cur.phash[0] = 0ull;
-      cur.tree[0] = 0;
-      cur.last[0] = -1;
-      cur.node[0] = -1;
-      cur.len[0] = 0;
-      s_n = 1;
-      s_nodes = 0;
+      sl[0].pb[0] = 0.0;
+      sl[0].pnb[0] = -INFINITY;
+      sl[0].tot[0] = 0.0;  // logaddexp(0, -inf)
+      sl[0].boost[0] = 0.0;
+      sl[0].hash[0] = 0ull;
+      sl[0].phash[0] = 0ull;
+      sl[0].tree[0] = 0;
+      sl[0].last[0] = -1;
+      sl[0].node[0] = -1;
+      sl[0].pnode[0] = -1;
+      sl[0].len[0] = 0;
     }
+    // live prefixes and trace nodes used: block-uniform registers, every
+    // thread counts the winners itself
+    int n = 1, nodes = 0;
     // frame 0's row and the root's closure record
     const float *lpb = a.lp + b * a.T * int64_t(V);
     if (Tb > 0)
@@ -157,6 +186,7 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
     asm volatile("cp.async.commit_group;" ::: "memory");
     __syncthreads();
     for (int64_t tf = 0; tf < Tb; ++tf) {
+      Slots &cur = sl[tf & 1], &nxt = sl[(tf + 1) & 1];
       const float *row = rows + (tf & 1) * Vp;
       int4 *s_rec = s_rec2[tf & 1];
       // prefetch the next frame's row into the other buffer (consumed after
@@ -174,46 +204,56 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
           for (int i = threadIdx.x; i < V; i += blockDim.x) nrow[i] = __ldg(src + i);
         }
       }
-      const int n = s_n;
-      // 2. parents, totals, carries (one thread per live prefix)
+      // 2. parents, carries and the carried prefixes' am (one thread per
+      // live prefix)
       if (threadIdx.x < n) {
         const int j = threadIdx.x;
-        const double tot = logaddexp(cur.pb[j], cur.pnb[j]);
-        s_tot[j] = tot;
+        const double tot = cur.tot[j];
         int par = -1;
         if (cur.len[j] > 0) {
+          const int pn = cur.pnode[j];
           for (int i = 0; i < n && par < 0; ++i)
             if (cur.len[i] == cur.len[j] - 1 && cur.hash[i] == cur.phash[j] &&
-                cb_same_tokens(np, nt, np[cur.node[j]], cur.node[i]))
+                (pn == cur.node[i] || cb_same_tokens(np, nt, pn, cur.node[i])))
               par = i;
         }
         s_par[j] = par;
-        s_cpb[j] = __dadd_rn(tot, static_cast<double>(row[a.blank]));
+        const double cpb = __dadd_rn(tot, static_cast<double>(row[a.blank]));
+        s_cpb[j] = cpb;
         double pnb = -INFINITY;
         if (cur.len[j] > 0) pnb = logaddexp(pnb, __dadd_rn(cur.pnb[j], static_cast<double>(row[cur.last[j]])));
         if (par >= 0) {
           // the parent's iteration (decoding.py:303-321): v = last_j
           const int v = cur.last[j];
-          double tot_i = logaddexp(cur.pb[par], cur.pnb[par]);
           const double contrib =
-              __dadd_rn(v == cur.last[par] ? cur.pb[par] : tot_i, static_cast<double>(row[v]));
+              __dadd_rn(v == cur.last[par] ? cur.pb[par] : cur.tot[par], static_cast<double>(row[v]));
           if (contrib != -INFINITY) pnb = logaddexp(pnb, contrib);
         }
         s_cpnb[j] = pnb;
+        s_amj[j] = logaddexp(cpb, pnb);
       }
       // exclusion bitmaps (extensions landing on a live prefix) and
       // closure records
       for (int i = threadIdx.x; i < n * Vw; i += blockDim.x) ex[i] = 0u;
       if (boost)
         for (int i = threadIdx.x; i < n * Vw; i += blockDim.x) bm[i] = 0u;
-      // this frame's closure records (issued last frame); the next row may pend
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      // this frame's closure records (issued last frame); the next row's
+      // group, the newest when one was issued this frame, may pend
+      if (kVec && tf + 1 < Tb)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
+      CB_MARK(0);
       if (threadIdx.x < n && s_par[threadIdx.x] >= 0) {
         const int v = cur.last[threadIdx.x];
         atomicOr(ex + s_par[threadIdx.x] * Vw + (v >> 5), 1u << (v & 31));
       }
       int total = 0;
+      // the thread's first closure entry stays in registers for the
+      // candidate pass (one load per entry when total <= blockDim.x)
+      int4 my_e = make_int4(0, 0, 0, 0);
+      int my_h = 0;
       if (boost) {
         for (int h = 0; h < n; ++h) total += s_rec[h].y;
         for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
@@ -222,15 +262,20 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
             off -= s_rec[h].y;
             ++h;
           }
-          const int tok = __ldg(&t.clo[s_rec[h].x + off].x);
-          atomicOr(bm + h * Vw + (tok >> 5), 1u << (tok & 31));
+          const int4 e = __ldg(t.clo + s_rec[h].x + off);
+          atomicOr(bm + h * Vw + (e.x >> 5), 1u << (e.x & 31));
+          if (idx == int(threadIdx.x)) {
+            my_e = e;
+            my_h = h;
+          }
         }
       }
       __syncthreads();
+      CB_MARK(1);
       // 3. new-prefix candidates
-      Cand list[K];
+      KCand list[K];
 #pragma unroll
-      for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+      for (int i = 0; i < K; ++i) list[i] = kcand_none();
       {
         // candidate (h, v): per-prefix values from shared memory
         auto dense = [&](int h, int v, float x) {
@@ -242,21 +287,70 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
           } else {
             bv = __dadd_rn(cur.boost[h], 0.0);
           }
-          const double amv = __dadd_rn(v == cur.last[h] ? cur.pb[h] : s_tot[h], static_cast<double>(x));
+          const double amv = __dadd_rn(v == cur.last[h] ? cur.pb[h] : cur.tot[h], static_cast<double>(x));
           if (amv == -INFINITY) return;
-          list_insert<K>(list, Cand{__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, h * V + v});
+          klist_insert<K>(list, kcand(__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, h * V + v));
         };
-        // work items (prefix, float4 chunk) spread over every thread
+        // work items (prefix, float4 chunk) spread over every thread; the
+        // prefix's values, the exclusion / closure bitmap nibbles and the
+        // root row's float4 are read once per item.  Float prefilter: each
+        // candidate's key is first estimated in fp32 (|error| <= 2^-21 M,
+        // M = the sum of the operands' magnitudes); a candidate whose estimate
+        // is below the warp's beam-th largest lane maximum by more than
+        // 2^-18 max M is strictly worse than `beam` candidates of its own
+        // warp, so it cannot be a winner and skips the exact fp64 key and the
+        // list insertion.  The survivors (a few per warp) are ranked exactly.
         if (kVec) {
           const int V4 = V >> 2, ni = n * V4;
           const float4 *r4 = reinterpret_cast<const float4 *>(row);
-          for (int it = threadIdx.x; it < ni; it += blockDim.x) {
-            const int h = it / V4, c = it - h * V4;
+          const float4 *q4 = reinterpret_cast<const float4 *>(root);
+          const float lamf = static_cast<float>(a.lam), alam = fabsf(lamf);
+          for (int it0 = threadIdx.x - lane; it0 < ni; it0 += blockDim.x) {  // warp-uniform trip count
+            const int it = it0 + lane;
+            const bool valid = it < ni;
+            const int h = valid ? it / V4 : 0, c = valid ? it - h * V4 : 0, v0 = 4 * c;
             const float4 x = r4[c];
-            dense(h, 4 * c, x.x);
-            dense(h, 4 * c + 1, x.y);
-            dense(h, 4 * c + 2, x.z);
-            dense(h, 4 * c + 3, x.w);
+            unsigned skip = valid ? (ex[h * Vw + (v0 >> 5)] >> (v0 & 31)) & 0xFu : 0xFu;
+            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+            float acc = 0.0f;
+            if (boost) {
+              skip |= (bm[h * Vw + (v0 >> 5)] >> (v0 & 31)) & 0xFu;
+              q = q4[c];
+              acc = __int_as_float(s_rec[h].z);
+            }
+            const double pbh = cur.pb[h], toth = cur.tot[h], bh = cur.boost[h];
+            const int lasth = cur.last[h];
+            const float pbf = static_cast<float>(pbh), totf = static_cast<float>(toth), bf = static_cast<float>(bh);
+            float f[4], lmax = -INFINITY, mmax = 0.0f;
+            auto est = [&](int k, float xv, float qv) {
+              const int v = v0 + k;
+              const float base = v == lasth ? pbf : totf, s = acc + qv;
+              float fk = (base + xv) + lamf * (bf + s);
+              const float mk = (fabsf(base) + fabsf(xv)) + alam * (fabsf(bf) + fabsf(s));
+              if (((skip >> k) & 1u) || v == a.blank) fk = -INFINITY;
+              f[k] = fk;
+              lmax = fmaxf(lmax, fk);
+              if (fk > -INFINITY) mmax = fmaxf(mmax, mk);
+            };
+            est(0, x.x, q.x);
+            est(1, x.y, q.y);
+            est(2, x.z, q.z);
+            est(3, x.w, q.w);
+            const float thr = warp_kth_max(lmax, beam);
+            const float mw = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mmax)));
+            const float cut = thr - mw * 0x1p-18f;
+            auto one = [&](int k, float xv, float qv) {
+              const int v = v0 + k;
+              if (((skip >> k) & 1u) || v == a.blank || f[k] < cut) return;
+              const double bv = __dadd_rn(bh, boost ? static_cast<double>(acc + qv) : 0.0);
+              const double amv = __dadd_rn(v == lasth ? pbh : toth, static_cast<double>(xv));
+              if (amv == -INFINITY) return;
+              klist_insert<K>(list, kcand(__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, h * V + v));
+            };
+            one(0, x.x, q.x);
+            one(1, x.y, q.y);
+            one(2, x.z, q.z);
+            one(3, x.w, q.w);
           }
         } else {
           for (int it = threadIdx.x; it < n * V; it += blockDim.x) {
@@ -265,38 +359,48 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
           }
         }
       }
+      CB_MARK(7);
       if (boost) {
         for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-          int h = 0, off = idx;
-          while (off >= s_rec[h].y) {
-            off -= s_rec[h].y;
-            ++h;
+          int h = my_h;
+          int4 e = my_e;
+          if (idx != int(threadIdx.x)) {
+            int off = idx;
+            h = 0;
+            while (off >= s_rec[h].y) {
+              off -= s_rec[h].y;
+              ++h;
+            }
+            e = __ldg(t.clo + s_rec[h].x + off);
           }
-          const int4 e = __ldg(t.clo + s_rec[h].x + off);
           const int v = e.x;
           if (v == a.blank || ((ex[h * Vw + (v >> 5)] >> (v & 31)) & 1u)) continue;
-          const double amv = __dadd_rn(v == cur.last[h] ? cur.pb[h] : s_tot[h], static_cast<double>(row[v]));
+          const double amv = __dadd_rn(v == cur.last[h] ? cur.pb[h] : cur.tot[h], static_cast<double>(row[v]));
           if (amv == -INFINITY) continue;
           const double bv = __dadd_rn(cur.boost[h], static_cast<double>(__int_as_float(e.z)));
-          list_insert<K>(list, Cand{__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, h * V + v});
+          klist_insert<K>(list, kcand(__dadd_rn(amv, __dmul_rn(a.lam, bv)), amv, h * V + v));
         }
       }
+      CB_MARK(8);
       // carried prefixes (cid past the extension range)
       if (threadIdx.x < n) {
         const int j = threadIdx.x;
-        const double amj = logaddexp(s_cpb[j], s_cpnb[j]);
-        list_insert<K>(list, Cand{__dadd_rn(amj, __dmul_rn(a.lam, cur.boost[j])), amj, kMaxTopK * V + j});
+        const double amj = s_amj[j];
+        klist_insert<K>(list, kcand(__dadd_rn(amj, __dmul_rn(a.lam, cur.boost[j])), amj, kMaxTopK * V + j));
       }
+      CB_MARK(2);
       // 4. top `beam` in two levels: each warp pops its own top from its
       // lanes' lists (shuffles only), then warp 0 merges the warps' lists
       for (int r = 0; r < beam; ++r) {
-        const Cand best = cand_warp_best(list[0]);
+        const KCand best = kc_warp_best(list[0]);
         if (lane == 0) s_wl[wid * beam + r] = best;
-        if (best.cid != INT_MAX && list[0].cid == best.cid) list_pop<K>(list);
+        if (best.cid != INT_MAX && list[0].cid == best.cid) klist_pop<K>(list);
       }
       __syncthreads();
-      if (wid == 0) merge_warp_lists(s_wl, int(blockDim.x >> 5), beam, lane, s_win, s_key, s_am);
+      CB_MARK(3);
+      if (wid == 0) kmerge_warp_lists(s_wl, int(blockDim.x >> 5), beam, lane, s_win, s_key, s_am);
       __syncthreads();
+      CB_MARK(4);
       // 5. the next beam
       if (threadIdx.x < beam) {
         const int r = threadIdx.x;
@@ -307,12 +411,14 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
             if (boost) cp_async16(&s_rec2[(tf + 1) & 1][r], t.clo_rec + cur.tree[j]);
             nxt.pb[r] = s_cpb[j];
             nxt.pnb[r] = s_cpnb[j];
+            nxt.tot[r] = s_am[r];  // = logaddexp(pb, pnb) (the candidate's am)
             nxt.boost[r] = cur.boost[j];
             nxt.hash[r] = cur.hash[j];
             nxt.phash[r] = cur.phash[j];
             nxt.tree[r] = cur.tree[j];
             nxt.last[r] = cur.last[j];
             nxt.node[r] = cur.node[j];
+            nxt.pnode[r] = cur.pnode[j];
             nxt.len[r] = cur.len[j];
           } else {
             const int h = cid / V, v = cid - h * V;
@@ -326,7 +432,7 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
             // rank order among the new prefixes
             int rank = 0;
             for (int q = 0; q < r; ++q) rank += s_win[q] != INT_MAX && s_win[q] < kMaxTopK * V;
-            const int node = s_nodes + rank;
+            const int node = nodes + rank;
             if (node < a.nmax) {
               a.tr_parent[nb + node] = cur.node[h];
               a.tr_token[nb + node] = v;
@@ -337,49 +443,45 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
             }
             nxt.pb[r] = -INFINITY;
             nxt.pnb[r] = s_am[r];
+            nxt.tot[r] = s_am[r];  // logaddexp(-inf, pnb)
             nxt.boost[r] = __dadd_rn(cur.boost[h], static_cast<double>(sc));
             nxt.hash[r] = cb_hash_push(cur.hash[h], v);
             nxt.phash[r] = cur.hash[h];
             nxt.tree[r] = nx;
             nxt.last[r] = v;
             nxt.node[r] = node < a.nmax ? node : -1;
+            nxt.pnode[r] = cur.node[h];
             nxt.len[r] = cur.len[h] + 1;
           }
         }
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
+      {  // every thread: the next beam's size and the trace nodes used
         int m = 0, e = 0;
         while (m < beam && s_win[m] != INT_MAX) {
           e += s_win[m] < kMaxTopK * V;
           ++m;
         }
-        s_n = m;
-        s_nodes += e;
-      }
-      if (threadIdx.x < beam) {
-        const int r = threadIdx.x;
-        cur.pb[r] = nxt.pb[r];
-        cur.pnb[r] = nxt.pnb[r];
-        cur.boost[r] = nxt.boost[r];
-        cur.hash[r] = nxt.hash[r];
-        cur.phash[r] = nxt.phash[r];
-        cur.tree[r] = nxt.tree[r];
-        cur.last[r] = nxt.last[r];
-        cur.node[r] = nxt.node[r];
-        cur.len[r] = nxt.len[r];
+        n = m;
+        nodes += e;
       }
       asm volatile("cp.async.commit_group;" ::: "memory");  // the next frame's records
       // the next row has landed (the records' group may still pend)
       asm volatile("cp.async.wait_group 1;" ::: "memory");
       __syncthreads();
+      CB_MARK(5);
+#ifdef PGPB_CB_PROFILE
+      if (blockIdx.x == 0 && threadIdx.x == 0) g_cb_prof[15] += 1;
+      __syncthreads();  // one bare barrier, for scale
+      CB_MARK(9);
+#endif
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     // final beam (rank order)
+    const Slots &cur = sl[Tb & 1];
     if (threadIdx.x < beam) {
       const int r = threadIdx.x;
       const int64_t o = b * beam + r;
-      if (r < s_n) {
+      if (r < n) {
         a.o_pb[o] = cur.pb[r];
         a.o_pnb[o] = cur.pnb[r];
         a.o_boost[o] = cur.boost[r];
@@ -388,13 +490,24 @@ __global__ void __launch_bounds__(cb_threads<K>()) ctc_beam_kernel(CbArgs a) {
         a.o_tree[o] = cur.tree[r];
       }
     }
-    if (threadIdx.x == 0) a.o_count[b] = s_n;
+    if (threadIdx.x == 0) a.o_count[b] = n;
   }
 }
 
 }  // namespace
 
 }  // namespace pgpb
+
+#ifdef PGPB_CB_PROFILE
+extern "C" int pgpb_debug_cb_profile(unsigned long long *out, int reset) {
+  PGPB_CUDA_TRY(cudaMemcpyFromSymbol(out, pgpb::g_cb_prof, sizeof(pgpb::g_cb_prof)));
+  if (reset) {
+    unsigned long long z[16] = {};
+    PGPB_CUDA_TRY(cudaMemcpyToSymbol(pgpb::g_cb_prof, z, sizeof(z)));
+  }
+  return PGPB_OK;
+}
+#endif
 
 extern "C" int pgpb_ctc_beam(const pgpb_table *table, const float *d_lp, int64_t B, int64_t T, int32_t V,
                              const int32_t *d_lengths, int32_t blank, int32_t beam, double lam, int32_t use_boost,
@@ -454,7 +567,8 @@ extern "C" int pgpb_ctc_beam(const pgpb_table *table, const float *d_lp, int64_t
                                      int(smem)));
   const int64_t cap = int64_t(sm_count(current_device())) * 2;
   const unsigned grid = unsigned(B < cap ? B : cap);
-  const int threads = beam <= 4 ? cb_threads<4>() : (beam <= 8 ? cb_threads<8>() : cb_threads<16>());
+  int threads = beam <= 4 ? cb_threads<4>() : (beam <= 8 ? cb_threads<8>() : cb_threads<16>());
+  if (tuning().cb_threads >= 32 && tuning().cb_threads <= threads) threads = tuning().cb_threads & ~31;
   fn<<<grid, threads, smem, static_cast<cudaStream_t>(stream)>>>(a);
   PGPB_CUDA_TRY(cudaGetLastError());
   return PGPB_OK;

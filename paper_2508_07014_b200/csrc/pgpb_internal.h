@@ -22,6 +22,7 @@ struct Tuning {
   int ll_warps = 0;       // label-loop step: warps (rows) per CTA
   int beam_blobs = 0;     // device beams: 0 advance blobs when built, 1 closure records + bitmap marking
   int adv_compact = 0;    // chained advance table layout: 0 by regime, 1 ranked bitmap, 2 compact arrays, 3 blobs
+  int cb_threads = 0;     // device CTC beam: threads per CTA (0 = by beam width)
 };
 Tuning &tuning();
 

@@ -59,6 +59,7 @@ int pgpb_set_tuning(const char *key, int32_t value) {
   else if (k == "ll.warps") t.ll_warps = value;
   else if (k == "adv.compact") t.adv_compact = value;
   else if (k == "beam.blobs") t.beam_blobs = value;
+  else if (k == "cb.threads") t.cb_threads = value;
   else return pgpb::fail(PGPB_EINVAL, "unknown tuning key " + k);
   return PGPB_OK;
 }
