@@ -113,7 +113,7 @@ template <int K, bool kVec>
 __device__ __forceinline__ void scan_candidates(const TableView &t, const float *root, const unsigned *bm,
                                                 int bm_words, const float *lp, int64_t ld, int64_t row0, int V,
                                                 const SBeam &s, const bool *expand, int beam, int skip, int special,
-                                                double lam, bool use_boost, const int4 *s_rec, Cand (&list)[K],
+                                                double lam, bool use_boost, const int4 *s_rec, KCand (&list)[K],
                                                 int t0 = 0, bool closure_pass = true) {
   const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
   // candidate (h, v) of token v at log-prob x (per-slot values from shared memory)
@@ -130,7 +130,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
       bv = boost_h;
     }
     const double amv = __dadd_rn(am_h, static_cast<double>(x));
-    list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + v});
+    klist_insert<K>(list, kcand(rank_key(amv, bv, lam), amv, h * V + v));
   };
   if (kVec) {
     // work items (slot, float4 chunk) spread over every thread; up to four
@@ -180,7 +180,7 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
       const float x = lp[(row0 + h) * ld + e.x];
       const double amv = __dadd_rn(s.am[h], static_cast<double>(x));
       const double bv = __dadd_rn(s.boost[h], static_cast<double>(__int_as_float(e.z)));
-      list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + e.x});
+      klist_insert<K>(list, kcand(rank_key(amv, bv, lam), amv, h * V + e.x));
     }
   }
 }
@@ -189,18 +189,18 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
 // lists with warp reductions, then warp 0 merges the warps' sorted k-lists head by head —
 // two block barriers in total instead of two per round.
 template <int K>
-__device__ __forceinline__ void block_topk(Cand (&list)[K], int k, Cand *s_warp, int *s_win, double *s_key,
+__device__ __forceinline__ void block_topk(KCand (&list)[K], int k, KCand *s_warp, int *s_win, double *s_key,
                                            double *s_am) {
   (void)s_warp;
-  __shared__ Cand s_wl[kDbMaxWarps * kMaxTopK];
+  __shared__ KCand s_wl[kDbMaxWarps * kMaxTopK];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = 0; r < k; ++r) {
-    const Cand best = cand_warp_best(list[0]);
+    const KCand best = kc_warp_best(list[0]);
     if (lane == 0) s_wl[wid * k + r] = best;
-    if (best.cid != INT_MAX && list[0].cid == best.cid) list_pop<K>(list);
+    if (best.cid != INT_MAX && list[0].cid == best.cid) klist_pop<K>(list);
   }
   __syncthreads();
-  if (wid == 0) merge_warp_lists(s_wl, nw, k, lane, s_win, s_key, s_am);
+  if (wid == 0) kmerge_warp_lists(s_wl, nw, k, lane, s_win, s_key, s_am);
   __syncthreads();
 }
 
@@ -245,7 +245,7 @@ template <int K>
 __device__ __forceinline__ void mark_and_score_closures(const TableView &t, unsigned *bm, int bm_words,
                                                         const SBeam &s, const bool *expand, int beam, int4 *s_rec,
                                                         const float *lp, int64_t ld, int64_t row0, int V, int skip,
-                                                        int special, double lam, Cand (&list)[K], int t0 = 0) {
+                                                        int special, double lam, KCand (&list)[K], int t0 = 0) {
   const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
   for (int i = tid; i < beam * bm_words; i += nt) bm[i] = 0u;
   for (int h = tid; h < beam; h += nt) s_rec[h] = expand[h] ? __ldg(t.clo_rec + s.tree[h]) : make_int4(0, 0, 0, 0);
@@ -264,7 +264,7 @@ __device__ __forceinline__ void mark_and_score_closures(const TableView &t, unsi
     const float x = lp[(row0 + h) * ld + e.x];
     const double amv = __dadd_rn(s.am[h], static_cast<double>(x));
     const double bv = __dadd_rn(s.boost[h], static_cast<double>(__int_as_float(e.z)));
-    list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + e.x});
+    klist_insert<K>(list, kcand(rank_key(amv, bv, lam), amv, h * V + e.x));
   }
   worker_sync(t0);
 }
@@ -303,7 +303,7 @@ template <int K>
 __device__ __forceinline__ void blob_closure_candidates(const TableView &t, const int4 *blobs, const SBeam &s,
                                                         const bool *expand, int beam, const float *lp, int64_t ld,
                                                         int64_t row0, int V, int skip, int special, double lam,
-                                                        Cand (&list)[K], int t0) {
+                                                        KCand (&list)[K], int t0) {
   const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
   const int S16 = t.adv_stride16, Vw = t.bits_words, E0 = t.adv_ent0;
   for (int i = tid; i < beam * Vw; i += nt) {
@@ -322,7 +322,7 @@ __device__ __forceinline__ void blob_closure_candidates(const TableView &t, cons
       const float x = lp[(row0 + h) * ld + v];
       const double amv = __dadd_rn(s.am[h], static_cast<double>(x));
       const double bv = __dadd_rn(s.boost[h], static_cast<double>(__int_as_float(e.y)));
-      list_insert<K>(list, Cand{rank_key(amv, bv, lam), amv, h * V + v});
+      klist_insert<K>(list, kcand(rank_key(amv, bv, lam), amv, h * V + v));
     }
   }
 }
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
   __shared__ SBeam s;
   __shared__ bool s_expand[kMaxTopK];
   __shared__ int4 s_rec[kMaxTopK];
-  __shared__ Cand s_warp[kDbMaxWarps];
+  __shared__ KCand s_warp[kDbMaxWarps];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
   __shared__ int s_node_base;
@@ -585,9 +585,9 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     // top-k barrier)
     const int bm_words = (V + 31) >> 5;
     const int t0 = blockDim.x > 32 ? 32 : 0;
-    Cand list[K];
+    KCand list[K];
 #pragma unroll
-    for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+    for (int i = 0; i < K; ++i) list[i] = kcand_none();
     int4 *blobs = (use_boost && a.blob_off) ? reinterpret_cast<int4 *>(smem + a.blob_off) : nullptr;
     if (int(threadIdx.x) >= t0) {
       if (blobs) {
@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(db_threads<K>()) aed_step_kernel(AedArgs a) {
   __shared__ SBeam s;
   __shared__ bool s_expand[kMaxTopK];
   __shared__ int4 s_rec[kMaxTopK];
-  __shared__ Cand s_warp[kDbMaxWarps];
+  __shared__ KCand s_warp[kDbMaxWarps];
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
   __shared__ int s_node_base, s_any;
@@ -767,9 +767,9 @@ __global__ void __launch_bounds__(db_threads<K>()) aed_step_kernel(AedArgs a) {
     return;
   }
   const int bm_words = (V + 31) >> 5;
-  Cand list[K];
+  KCand list[K];
 #pragma unroll
-  for (int i = 0; i < K; ++i) list[i] = Cand{-INFINITY, -INFINITY, INT_MAX};
+  for (int i = 0; i < K; ++i) list[i] = kcand_none();
   if (use_boost)
     mark_and_score_closures<K>(tv, bm, bm_words, s, s_expand, beam, s_rec, a.lp, a.ld, hb, V, -1, eos, a.lam, list);
   scan_candidates<K, kVec>(tv, root, bm, bm_words, a.lp, a.ld, hb, V, s, s_expand, beam, -1, eos, a.lam, use_boost,
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(db_threads<K>()) aed_step_kernel(AedArgs a) {
   // carried hypotheses (ended or at max_len), ranked unchanged
   for (int h = threadIdx.x; h < beam; h += blockDim.x)
     if ((s.flags[h] & kValid) && !s_expand[h])
-      list_insert<K>(list, Cand{rank_key(s.am[h], s.boost[h], a.lam), s.am[h], beam * V + h});
+      klist_insert<K>(list, kcand(rank_key(s.am[h], s.boost[h], a.lam), s.am[h], beam * V + h));
   block_topk<K>(list, beam, s_warp, s_win, s_key, s_am);
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
