@@ -52,9 +52,21 @@ __device__ unsigned long long g_tb_prof[16];
       tb_last = now_;                                                               \
     }                                                                               \
   } while (0)
+// the first expansion thread's timeline (thread 32)
+#define TB_MARKW(i)                                                                 \
+  do {                                                                              \
+    if (blockIdx.x == 0 && threadIdx.x == 32) {                                     \
+      const long long now_ = clock64();                                             \
+      atomicAdd(&g_tb_prof[i], (unsigned long long)(now_ - tb_lastw));            \
+      tb_lastw = now_;                                                              \
+    }                                                                               \
+  } while (0)
 #else
 #define TB_MARK(i) \
   do {             \
+  } while (0)
+#define TB_MARKW(i) \
+  do {              \
   } while (0)
 #endif
 
@@ -427,7 +439,7 @@ template <int K, bool kVec>
 __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
 #ifdef PGPB_TBEAM_PROFILE
-  long long tb_last = clock64();
+  long long tb_last = clock64(), tb_lastw = tb_last;
 #endif
   __shared__ SBeam s;
   __shared__ bool s_expand[kMaxTopK];
@@ -591,24 +603,33 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     int4 *blobs = (use_boost && a.blob_off) ? reinterpret_cast<int4 *>(smem + a.blob_off) : nullptr;
     if (int(threadIdx.x) >= t0) {
       if (blobs) {
+        TB_MARKW(7);
         load_blobs(tv, blobs, s, s_expand, beam, s_rec, t0);
+        TB_MARKW(8);
         blob_closure_candidates<K>(tv, blobs, s, s_expand, beam, LP, LD, R0, V, a.blank, -1, a.lam, list, t0);
         TB_MARK(2);
+        TB_MARKW(9);
         // the blobs' closure words are the dense scan's exclusion bitmaps
         scan_candidates<K, kVec>(tv, root, reinterpret_cast<const unsigned *>(blobs) + 4, tv.adv_stride16 * 4, LP,
                                  LD, R0, V, s, s_expand, beam, a.blank, -1, a.lam, use_boost, s_rec, list, t0, false);
+        TB_MARKW(10);
       } else {
         if (use_boost)
           mark_and_score_closures<K>(tv, bm, bm_words, s, s_expand, beam, s_rec, LP, LD, R0, V, a.blank, -1, a.lam,
                                      list, t0);
         TB_MARK(2);
+        TB_MARKW(7);
+        TB_MARKW(8);
+        TB_MARKW(9);
         scan_candidates<K, kVec>(tv, root, bm, bm_words, LP, LD, R0, V, s, s_expand, beam, a.blank, -1, a.lam,
                                  use_boost, s_rec, list, t0, false);
+        TB_MARKW(10);
       }
     }
     TB_MARK(3);
     block_topk<K>(list, beam, s_warp, s_win, s_key, s_am);
     TB_MARK(4);
+    TB_MARKW(11);
     for (int r = threadIdx.x; r < beam; r += blockDim.x) {
       const int cid = s_win[r];
       const int64_t o = hb + r;

@@ -34,3 +34,5 @@ for lam in (0.0, 1.0):
     waves = c["T"] * 6
     names = ["stage", "merge", "mark", "scan", "topk", "winners"]
     print("lam", lam, {n: round(int(buf[i]) / waves / 1.965e3, 2) for i, n in enumerate(names)}, "us per wave (CTA 0)")
+    wn = ["w:to-expansion", "w:blobs", "w:closure", "w:scan", "w:topk"]
+    print("  thread 32:", {n: round(int(buf[7 + i]) / waves / 1.965e3, 2) for i, n in enumerate(wn)})
