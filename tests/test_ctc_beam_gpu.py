@@ -113,3 +113,32 @@ def test_ctc_beam_batch_rollback_extension():
                          want_trace=True)
     for b in range(4):
         _cmp(out[b][1], orc.ctc_beam(lps[b], 0, tab, 1.0, 4, rollback=True))
+
+
+@pytest.mark.parametrize("beam", [4, 8])
+def test_ctc_beam_batch_masked_rows(beam):
+    """Rows with most tokens at -inf (fewer finite candidates per warp than
+    the beam, so the fp32 prefilter's warp bound is -inf) and a few frames
+    where only blank is finite; boosted and unboosted vs the oracle."""
+    from paper_2508_07014_b200 import DecodeConfig
+    from paper_2508_07014_b200.beams import ctc_beam_batch
+
+    phrases, V = gi.corpus("p20k_v1024")
+    tab = product_table(phrases, V)
+    rng = np.random.default_rng(70 + beam)
+    B, T = 4, 16
+    lps = np.stack([gi.random_emissions(rng, T, V) for _ in range(B)])
+    for b in range(B):
+        for t in range(T):
+            keep = rng.choice(V, size=int(rng.integers(1, 9)), replace=False)
+            row = np.full(V, -np.inf, np.float32)
+            row[keep] = lps[b, t, keep]
+            row[0] = lps[b, t, 0]
+            if t % 5 == 4:
+                row[1:] = -np.inf
+            lps[b, t] = row
+    lens = np.array([T, T - 1, 2, 1], np.int32)
+    for lam in (1.0, 0.0):
+        out = ctc_beam_batch(lps, lens, tab, DecodeConfig(lam=lam, beam_size=beam), blank_id=0, want_trace=True)
+        for b in range(B):
+            _cmp(out[b][1], orc.ctc_beam(lps[b, :lens[b]], 0, tab, lam, beam))
