@@ -371,6 +371,25 @@ __device__ __forceinline__ void setup_root(const TableView &t, bool use_boost, i
   bm = reinterpret_cast<unsigned *>(smem + off);
 }
 
+// setup_root with the root row brought in by cp.async (the caller waits for
+// its group before the barrier that precedes the first read), so no warp
+// stalls on it.
+__device__ __forceinline__ void setup_root_async(const TableView &t, bool use_boost, int smem_root,
+                                                 unsigned char *smem, const float *&root, unsigned *&bm) {
+  root = t.root_scores;
+  size_t off = 0;
+  if (use_boost && smem_root) {
+    float *s_root = reinterpret_cast<float *>(smem);
+    const int n4 = t.vocab_padded >> 2;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x)
+      db_cp_async16(reinterpret_cast<float4 *>(s_root) + i, reinterpret_cast<const float4 *>(t.root_scores) + i);
+    root = s_root;
+    off = size_t(t.vocab_padded) * 4;
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  bm = reinterpret_cast<unsigned *>(smem + off);
+}
+
 // ---------------------------------------------------------------------------
 // Transducer wave
 
@@ -460,7 +479,30 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
   const int32_t *np = S.trace.parent + nb, *nt = S.trace.token + nb;
   const float *root;
   unsigned *bm;
-  setup_root(tv, use_boost, a.smem_root, smem, root, bm);
+  setup_root_async(tv, use_boost, a.smem_root, smem, root, bm);
+  // the beam's slots staged by the last warp, off the log-softmax warps'
+  // path (their global round trips overlap)
+  const bool expand_wave = a.wave < S.cap;
+  {
+    const int w0 = int(blockDim.x) - 32;
+    if (int(threadIdx.x) >= w0) {
+      const int l = int(threadIdx.x) - w0;
+      for (int h = l; h < beam; h += 32) {
+        s.am[h] = S.hyps.am[hb + h];
+        s.boost[h] = S.hyps.boost[hb + h];
+        s.tree[h] = S.hyps.tree[hb + h];
+        s.last[h] = S.hyps.last[hb + h];
+        s.node[h] = S.hyps.node[hb + h];
+        s.len[h] = S.hyps.len[hb + h];
+        s.hash[h] = S.hyps.hash[hb + h];
+        const uint8_t f = S.hyps.flags[hb + h];
+        s.flags[h] = f;
+        s.extra[h] = 0.0;
+        s_expand[h] = expand_wave && (f & kValid);
+      }
+      if (l == 0) s_node_base = S.trace.count[b];
+    }
+  }
   // log-prob rows of the beam slots: the caller's f32 rows, or (fused) the
   // slots' logits log-softmaxed into shared memory after the bitmaps, one
   // warp per row, torch's formula order (as log_softmax_bf16_kernel)
@@ -494,10 +536,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     LD = Vp4;
     R0 = 0;
   }
-  stage_beam(S.hyps, hb, beam, s);
-  const bool expand_wave = a.wave < S.cap;
-  for (int h = threadIdx.x; h < beam; h += blockDim.x) s_expand[h] = expand_wave && (s.flags[h] & kValid);
-  if (threadIdx.x == 0) s_node_base = S.trace.count[b];
+  asm volatile("cp.async.wait_group 0;" ::: "memory");  // the root row
   __syncthreads();
 
   TB_MARK(0);
