@@ -517,6 +517,38 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
       const __nv_bfloat16 *xr = a.logits + (hb + r) * a.ld_logits;
       float *yr = lrows + size_t(r) * Vp4;
       float *gr = const_cast<float *>(a.lp) + (hb + r) * a.ld;
+      if (V <= 1024) {
+        // the row's 32 values per lane loaded once, all in flight together;
+        // same per-lane order (v = lane + 32 k) and reductions as below
+        float xv[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int v = lane + 32 * k;
+          xv[k] = v < V ? __bfloat162float(xr[v]) : -INFINITY;
+        }
+        float m = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) m = fmaxf(m, xv[k]);
+        float mr;
+        asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(m));
+        float sm = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (lane + 32 * k < V) sm += expf(xv[k] - mr);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(kFull, sm, o);
+        const float ls = logf(sm);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int v = lane + 32 * k;
+          if (v < V) {
+            const float y = (xv[k] - mr) - ls;
+            yr[v] = y;
+            gr[v] = y;
+          }
+        }
+        continue;
+      }
       float m = -INFINITY;
       for (int v = lane; v < V; v += 32) m = fmaxf(m, __bfloat162float(xr[v]));
       float mr;
