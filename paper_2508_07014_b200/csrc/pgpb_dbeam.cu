@@ -291,24 +291,6 @@ __device__ __forceinline__ void db_cp_async16(void *dst, const void *src) {
                : "memory");
 }
 
-// Copy the expandable slots' blobs, then publish {0, count, acc, 0} per slot
-// in s_rec (zero for slots that do not expand).  Worker threads [t0, ..).
-__device__ __forceinline__ void load_blobs(const TableView &t, int4 *blobs, const SBeam &s, const bool *expand,
-                                           int beam, int4 *s_rec, int t0) {
-  const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0, S16 = t.adv_stride16;
-  for (int i = tid; i < beam * S16; i += nt) {
-    const int h = i / S16;
-    if (expand[h]) db_cp_async16(blobs + i, t.adv_blob + int64_t(s.tree[h]) * S16 + (i - h * S16));
-  }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-  worker_sync(t0);
-  for (int h = tid; h < beam; h += nt) {
-    const int32_t *bl = reinterpret_cast<const int32_t *>(blobs + size_t(h) * S16);
-    s_rec[h] = expand[h] ? make_int4(0, bl[1], bl[0], 0) : make_int4(0, 0, 0, 0);
-  }
-  worker_sync(t0);
-}
-
 // Closure candidates of the expandable slots from their blobs: every set
 // bit of a slot's closure words is a first-hit arc, its pair the rank-th.
 template <int K>
@@ -501,6 +483,23 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
         s_expand[h] = expand_wave && (f & kValid);
       }
       if (l == 0) s_node_base = S.trace.count[b];
+      if (use_boost && a.blob_off && expand_wave) {
+        // the expandable slots' advance blobs, copied while warps 0.. run
+        // the log-softmax; their headers give the closure records
+        __syncwarp();
+        int4 *bl = reinterpret_cast<int4 *>(smem + a.blob_off);
+        const int S16 = tv.adv_stride16;
+        for (int i = l; i < beam * S16; i += 32) {
+          const int h = i / S16;
+          if (s_expand[h]) db_cp_async16(bl + i, tv.adv_blob + int64_t(s.tree[h]) * S16 + (i - h * S16));
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        for (int h = l; h < beam; h += 32) {
+          const int32_t *hd = reinterpret_cast<const int32_t *>(bl + size_t(h) * S16);
+          s_rec[h] = s_expand[h] ? make_int4(0, hd[1], hd[0], 0) : make_int4(0, 0, 0, 0);
+        }
+      }
     }
   }
   // log-prob rows of the beam slots: the caller's f32 rows, or (fused) the
@@ -675,8 +674,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     if (int(threadIdx.x) >= t0) {
       if (blobs) {
         TB_MARKW(7);
-        load_blobs(tv, blobs, s, s_expand, beam, s_rec, t0);
-        TB_MARKW(8);
+        TB_MARKW(8);  // blobs and their records staged before the block barrier
         blob_closure_candidates<K>(tv, blobs, s, s_expand, beam, LP, LD, R0, V, a.blank, -1, a.lam, list, t0);
         TB_MARK(2);
         TB_MARKW(9);
