@@ -298,7 +298,9 @@ __device__ __forceinline__ void blob_closure_candidates(const TableView &t, cons
                                                         const bool *expand, int beam, const float *lp, int64_t ld,
                                                         int64_t row0, int V, int skip, int special, double lam,
                                                         KCand (&list)[K], int t0) {
-  const int tid = int(threadIdx.x) - t0, nt = int(blockDim.x) - t0;
+  // items from the last worker thread down: the dense scan gives its extra
+  // items to the first worker threads, so the two loads do not stack up
+  const int nt = int(blockDim.x) - t0, tid = nt - 1 - (int(threadIdx.x) - t0);
   const int S16 = t.adv_stride16, Vw = t.bits_words, E0 = t.adv_ent0;
   for (int i = tid; i < beam * Vw; i += nt) {
     const int h = i / Vw, w = i - h * Vw;
