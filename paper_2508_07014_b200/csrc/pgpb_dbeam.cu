@@ -161,10 +161,37 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
       for (int g = 0; g < 4; ++g) {
         const int it = i0 + g * nt, h = it / V4, c = it - h * V4;
         if (it < n && expand[h]) {
-          dense(h, 4 * c, xs[g].x);
-          dense(h, 4 * c + 1, xs[g].y);
-          dense(h, 4 * c + 2, xs[g].z);
-          dense(h, 4 * c + 3, xs[g].w);
+          // the item's closure-bitmap nibble, root float4 and slot values
+          // read once (dense() re-reads them per token)
+          const int v0 = 4 * c;
+          const double am_h = s.am[h], boost_h = s.boost[h];
+          unsigned cb = 0u;
+          float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+          float acc = 0.0f;
+          if (use_boost) {
+            cb = (bm[h * bm_words + (v0 >> 5)] >> (v0 & 31)) & 0xFu;
+            q = reinterpret_cast<const float4 *>(root)[c];
+            acc = __int_as_float(s_rec[h].z);
+          }
+          auto one = [&](int k, float x, float r) {
+            const int v = v0 + k;
+            if (v == skip) return;
+            double bv;
+            if (v == special) {
+              bv = __dadd_rn(boost_h, s.extra[h]);
+            } else if (use_boost) {
+              if ((cb >> k) & 1u) return;
+              bv = __dadd_rn(boost_h, static_cast<double>(acc + r));
+            } else {
+              bv = boost_h;
+            }
+            const double amv = __dadd_rn(am_h, static_cast<double>(x));
+            klist_insert<K>(list, kcand(rank_key(amv, bv, lam), amv, h * V + v));
+          };
+          one(0, xs[g].x, q.x);
+          one(1, xs[g].y, q.y);
+          one(2, xs[g].z, q.z);
+          one(3, xs[g].w, q.w);
         }
       }
     }
