@@ -465,6 +465,9 @@ __device__ __forceinline__ void tbeam_joint_hidden(const TBeamArgs &a, int b, in
   }
 }
 
+// Fused log-softmax split: warps per row, values per warp.
+constexpr int kLsParts = 7, kLsPart = 160;
+
 template <int K, bool kVec>
 __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -522,15 +525,11 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
           const int h = i / S16;
           if (s_expand[h]) db_cp_async16(bl + i, tv.adv_blob + int64_t(s.tree[h]) * S16 + (i - h * S16));
         }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
-        for (int h = l; h < beam; h += 32) {
-          const int32_t *hd = reinterpret_cast<const int32_t *>(bl + size_t(h) * S16);
-          s_rec[h] = s_expand[h] ? make_int4(0, hd[1], hd[0], 0) : make_int4(0, 0, 0, 0);
-        }
+        asm volatile("cp.async.commit_group;" ::: "memory");  // waited for before the stage barrier
       }
     }
   }
+  const bool staged_blobs = use_boost && a.blob_off && expand_wave;
   // log-prob rows of the beam slots: the caller's f32 rows, or (fused) the
   // slots' logits log-softmaxed into shared memory after the bitmaps, one
   // warp per row, torch's formula order (as log_softmax_bf16_kernel)
@@ -541,6 +540,57 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     float *lrows = reinterpret_cast<float *>(
         (reinterpret_cast<uintptr_t>(bm + size_t(beam) * ((V + 31) >> 5)) + 15) & ~uintptr_t(15));
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (V <= kLsParts * kLsPart && beam * kLsParts <= nw - 1) {
+      // each row over kLsParts warps (kLsPart values each, 5 per lane):
+      // partial maxima and sums through shared memory, summed in part
+      // order; the last warp stays free for the slot staging
+      __shared__ float s_pmax[kMaxTopK * kLsParts], s_psum[kMaxTopK * kLsParts];
+      const int w = threadIdx.x >> 5, r = w / kLsParts, part = w - r * kLsParts;
+      const bool mine = r < beam;
+      float xv[kLsPart / 32];
+      const __nv_bfloat16 *xr = a.logits + (hb + (mine ? r : 0)) * a.ld_logits;
+      if (mine) {
+        float m = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < kLsPart / 32; ++k) {
+          const int v = part * kLsPart + 32 * k + lane;
+          xv[k] = v < V ? __bfloat162float(xr[v]) : -INFINITY;
+          m = fmaxf(m, xv[k]);
+        }
+        float mr;
+        asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(m));
+        if (lane == 0) s_pmax[w] = mr;
+      }
+      __syncthreads();
+      float rmax = -INFINITY;
+      if (mine) {
+        for (int q = 0; q < kLsParts; ++q) rmax = fmaxf(rmax, s_pmax[r * kLsParts + q]);
+        float sm = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kLsPart / 32; ++k)
+          if (part * kLsPart + 32 * k + lane < V) sm += expf(xv[k] - rmax);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(kFull, sm, o);
+        if (lane == 0) s_psum[w] = sm;
+      }
+      __syncthreads();
+      if (mine) {
+        float tot = 0.0f;
+        for (int q = 0; q < kLsParts; ++q) tot += s_psum[r * kLsParts + q];
+        const float ls = logf(tot);
+        float *yr = lrows + size_t(r) * Vp4;
+        float *gr = const_cast<float *>(a.lp) + (hb + r) * a.ld;
+#pragma unroll
+        for (int k = 0; k < kLsPart / 32; ++k) {
+          const int v = part * kLsPart + 32 * k + lane;
+          if (v < V) {
+            const float y = (xv[k] - rmax) - ls;
+            yr[v] = y;
+            gr[v] = y;
+          }
+        }
+      }
+    } else
     for (int r = threadIdx.x >> 5; r < beam; r += nw) {
       const __nv_bfloat16 *xr = a.logits + (hb + r) * a.ld_logits;
       float *yr = lrows + size_t(r) * Vp4;
@@ -596,7 +646,15 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     LD = Vp4;
     R0 = 0;
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");  // the root row
+  asm volatile("cp.async.wait_group 0;" ::: "memory");  // the root row (and the staging warp's blobs)
+  if (staged_blobs && int(threadIdx.x) >= int(blockDim.x) - 32) {
+    __syncwarp();
+    const int4 *bl = reinterpret_cast<const int4 *>(smem + a.blob_off);
+    for (int h = int(threadIdx.x) - (int(blockDim.x) - 32); h < beam; h += 32) {
+      const int32_t *hd = reinterpret_cast<const int32_t *>(bl + size_t(h) * tv.adv_stride16);
+      s_rec[h] = s_expand[h] ? make_int4(0, hd[1], hd[0], 0) : make_int4(0, 0, 0, 0);
+    }
+  }
   __syncthreads();
 
   TB_MARK(0);
