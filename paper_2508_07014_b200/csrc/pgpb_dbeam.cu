@@ -145,32 +145,34 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
     klist_insert<K>(list, kcand(rank_key(amv, bv, lam), amv, h * V + v));
   };
   if (kVec) {
-    // work items (slot, float4 chunk) spread over every thread; up to four
-    // items' loads in flight before any is scored
-    const int V4 = V >> 2;
-    const int n = beam * V4;
+    // work items (slot, float2 pair) spread over every thread (pairs, not
+    // float4s: 2048 items over the 992 worker threads leave at most 6 tokens
+    // on a thread instead of 8); up to four items' loads in flight before
+    // any is scored
+    const int V2 = V >> 1;
+    const int n = beam * V2;
     for (int i0 = tid; i0 < n; i0 += 4 * nt) {
-      float4 xs[4];
+      float2 xs[4];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        const int it = i0 + g * nt, h = it / V4;
+        const int it = i0 + g * nt, h = it / V2;
         // generic loads: the rows are global (caller's) or shared (fused log-softmax)
-        if (it < n && expand[h]) xs[g] = reinterpret_cast<const float4 *>(lp + (row0 + h) * ld)[it - h * V4];
+        if (it < n && expand[h]) xs[g] = reinterpret_cast<const float2 *>(lp + (row0 + h) * ld)[it - h * V2];
       }
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
-        const int it = i0 + g * nt, h = it / V4, c = it - h * V4;
+        const int it = i0 + g * nt, h = it / V2, c = it - h * V2;
         if (it < n && expand[h]) {
-          // the item's closure-bitmap nibble, root float4 and slot values
-          // read once (dense() re-reads them per token)
-          const int v0 = 4 * c;
+          // the item's closure-bitmap bits, root pair and slot values read
+          // once (dense() re-reads them per token)
+          const int v0 = 2 * c;
           const double am_h = s.am[h], boost_h = s.boost[h];
           unsigned cb = 0u;
-          float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+          float2 q = make_float2(0.f, 0.f);
           float acc = 0.0f;
           if (use_boost) {
-            cb = (bm[h * bm_words + (v0 >> 5)] >> (v0 & 31)) & 0xFu;
-            q = reinterpret_cast<const float4 *>(root)[c];
+            cb = (bm[h * bm_words + (v0 >> 5)] >> (v0 & 31)) & 0x3u;
+            q = reinterpret_cast<const float2 *>(root)[c];
             acc = __int_as_float(s_rec[h].z);
           }
           auto one = [&](int k, float x, float r) {
@@ -190,8 +192,6 @@ __device__ __forceinline__ void scan_candidates(const TableView &t, const float 
           };
           one(0, xs[g].x, q.x);
           one(1, xs[g].y, q.y);
-          one(2, xs[g].z, q.z);
-          one(3, xs[g].w, q.w);
         }
       }
     }
