@@ -446,18 +446,21 @@ __device__ __forceinline__ void write_hyp(const pgpb_beam_hyps &H, int64_t i, do
 // = the slot's last token (blank at the start), as beam_hidden_kernel.  The
 // hypotheses and t were just written by this block (visible after the
 // barrier; read through L2).
-__device__ __forceinline__ void tbeam_joint_hidden(const TBeamArgs &a, int b, int64_t hb, int beam) {
+// tf: the frame the next wave reads (this kernel's S.t[b] after its update);
+// s_ctx[k]: slot k's last token as this kernel wrote it, INT_MIN where it
+// kept the stored one (read back from global)
+__device__ __forceinline__ void tbeam_joint_hidden(const TBeamArgs &a, int b, int64_t hb, int beam, int tf,
+                                                   const int *s_ctx) {
   __syncthreads();
   const pgpb_tbeam_state &S = a.s;
   const int len = S.lengths[b];
-  int tf = __ldcg(S.t + b);
   const int lim = len > 0 ? len - 1 : 0;
   if (tf > lim) tf = lim;
   const int J = a.J;
   const __nv_bfloat16 *e = a.enc + int64_t(b) * a.enc_ld_b + int64_t(tf) * J;
   for (int i = threadIdx.x; i < beam * J; i += blockDim.x) {
     const int k = i / J, j = i - k * J;
-    const int lst = __ldcg(S.hyps.last + hb + k);
+    const int lst = s_ctx[k] != INT_MIN ? s_ctx[k] : __ldcg(S.hyps.last + hb + k);
     const int ctx = lst < 0 ? a.blank : lst;
     const float sv = __bfloat162float(__float2bfloat16_rn(__bfloat162float(e[j]) +
                                                           __bfloat162float(a.pred_j[int64_t(ctx) * J + j])));
@@ -481,6 +484,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
   __shared__ int s_win[kMaxTopK];
   __shared__ double s_key[kMaxTopK], s_am[kMaxTopK];
   __shared__ int s_node_base;
+  __shared__ int s_ctx[kMaxTopK];
   const pgpb_tbeam_state &S = a.s;
   const int b = blockIdx.x;
   const int t = S.t[b];
@@ -789,6 +793,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
     for (int r = threadIdx.x; r < beam; r += blockDim.x) {
       const int cid = s_win[r];
       const int64_t o = hb + r;
+      s_ctx[r] = INT_MIN;
       if (cid == INT_MAX) {
         S.hyps.flags[o] = 0;
         continue;
@@ -812,6 +817,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
       S.trace.delta[nb + node] = static_cast<double>(sc);
       write_hyp(S.hyps, o, s_am[r], __dadd_rn(s.boost[h], static_cast<double>(sc)), nx, v, node, s.len[h] + 1,
                 hash_push(s.hash[h], v), kValid);
+      s_ctx[r] = v;
     }
     if (threadIdx.x == 0) {
       int n = 0;
@@ -820,7 +826,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
       S.trace.count[b] = int(s_node_base + n < lim ? s_node_base + n : lim);
     }
     TB_MARK(5);
-    if (a.z) tbeam_joint_hidden(a, b, hb, beam);
+    if (a.z) tbeam_joint_hidden(a, b, hb, beam, t, s_ctx);
     return;
   }
 
@@ -865,12 +871,15 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
       if (bj != INT_MAX && (bj & 31) == lane) taken |= 1ull << (bj >> 5);
       if (lane == 0) {
         const int64_t o = hb + r;
+        s_ctx[r] = INT_MIN;
         if (bj == INT_MAX) {
           S.hyps.flags[o] = 0;
         } else {
           const int64_t q = pb + bj;
-          write_hyp(S.hyps, o, S.pool.am[q], S.pool.boost[q], S.pool.tree[q], S.pool.last[q], S.pool.node[q],
+          const int lq = S.pool.last[q];
+          write_hyp(S.hyps, o, S.pool.am[q], S.pool.boost[q], S.pool.tree[q], lq, S.pool.node[q],
                     S.pool.len[q], S.pool.hash[q], kValid);
+          s_ctx[r] = lq;
         }
       }
     }
@@ -879,7 +888,7 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
       S.t[b] = t + 1;
     }
   }
-  if (a.z) tbeam_joint_hidden(a, b, hb, beam);
+  if (a.z) tbeam_joint_hidden(a, b, hb, beam, t + 1, s_ctx);
 }
 
 // ---------------------------------------------------------------------------
