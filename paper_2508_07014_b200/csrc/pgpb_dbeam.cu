@@ -535,8 +535,12 @@ __global__ void __launch_bounds__(db_threads<K>()) tbeam_wave_kernel(TBeamArgs a
   }
   const bool staged_blobs = use_boost && a.blob_off && expand_wave;
   // log-prob rows of the beam slots: the caller's f32 rows, or (fused) the
-  // slots' logits log-softmaxed into shared memory after the bitmaps, one
-  // warp per row, torch's formula order (as log_softmax_bf16_kernel)
+  // slots' logits log-softmaxed into shared memory after the bitmaps with
+  // torch's formula, (x - max) - log(sum exp(x - max)): 7 warps per row
+  // (partial maxima and sums through shared memory, summed in part order)
+  // for V <= 1120 and beams <= 4, else one warp per row in the order of
+  // log_softmax_bf16_kernel.  Either way the rows are written to lp as the
+  // record of what was decided on (the replay tests decode those rows).
   const float *LP = a.lp;
   int64_t LD = a.ld, R0 = hb;
   if (a.logits) {
