@@ -72,6 +72,13 @@ mem = torch.randn((3, 5, 32), device=dev)
 AEDBeamDecoder(amodel, tab, pb.DecodeConfig(lam=1.0, beam_size=4), 3, max_len=5, eos=V - 1, use_graph=False).decode(mem)
 AEDGreedyDecoder(amodel, tab, pb.DecodeConfig(lam=1.0, beam_size=1), 3, max_len=5, eos=V - 1,
                  use_graph=False).decode(mem)
+# device CTC prefix beam (pgpb_ctc_beam), boosted and not, ragged lengths
+from paper_2508_07014_b200.beams import ctc_beam_batch  # noqa: E402
+
+lps = np.stack([gi.random_emissions(rng, 10, V) for _ in range(3)])
+for lam in (1.0, 0.0):
+    out = ctc_beam_batch(lps, np.array([10, 1, 6], np.int32), tab, pb.DecodeConfig(lam=lam, beam_size=4), blank_id=0)
+    assert [h.tokens for h in out[0][1]] == [h["tokens"] for h in orc.ctc_beam(lps[0], 0, tab, lam, 4)]
 # keyphrase hits on the device
 from paper_2508_07014_b200.evaluation import keyphrase_hits_device  # noqa: E402
 
