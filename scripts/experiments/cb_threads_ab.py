@@ -21,7 +21,7 @@ for rep in range(2):
     for thr, sc in [(t, c) for t in thr_list for c in scores]:
         _lib.set_tuning("cb.threads", thr)
         if "CB_SCORES" in os.environ:
-            _lib.set_tuning("cb.scores", sc)  # only in builds that have the key
+            _lib.set_tuning(os.environ.get("CB_KEY", "cb.scores"), sc)  # only in builds that have the key
         r = bench.bench_ctc_beam(tab, V, torch.device("cuda", 0), 0, 1)
         for k, v in r.items():
             if isinstance(v, dict) and "overhead" in v:
